@@ -1,0 +1,406 @@
+#!/usr/bin/env python
+"""Benchmark: fp64 NE-GS sweep throughput (DOF-updates/s) on Poisson control.
+
+Headline workload (BASELINE.json configs[2], the north_star target): level 12
+(4097 x 4097 P1 nodes, 33,570,818 unknowns, fp64, alpha = 1e-6), one step =
+one forward NE-GS sweep in the reference's order (wavefront mode) over the
+finest level, x and r resident in HBM (537 MB > the 126 MB L2, so no flush
+is needed between steps).  Also reported: every hot kernel of the cycle on
+the same level, the time to 1e-8 of a multigrid solve, the end-to-end sweep
+through the public API with host buffers, the CPU oracle on the host, and
+the clocks seen during the timed region.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Multi-GPU (torchrun, one rank per GPU): every rank sweeps its own level-12
+replica ("replicas only" for the exact-order sweep); time is
+the max over ranks, value the whole-job throughput.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("fp64 DOF-updates/s per NE-GS sweep; multigrid time to 1e-8 rel. "
+          "residual")
+UNIT = "DOF-updates/s"
+# algorithmic HBM bytes per unknown
+BYTES = {"ne_gs": 32, "ne_jacobi": 56, "residual": 24, "restrict": 10,
+         "prolong": 18}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [],
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        backend = os.environ.get("OCMG_BENCH_BACKEND", "nccl")
+        dist.init_process_group(backend)
+    return ws, rank, local
+
+
+def max_over_ranks(v, ws, device):
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle (reported baseline / reference arm)
+# ---------------------------------------------------------------------------
+
+def cpu_sweep_rate(level=10, sweeps=10, alpha=1e-6):
+    """Oracle C port of kernels.lsgs_sweep (1 thread) on a seeded level."""
+    import oracle as O
+    osys = O.poisson_system(level, alpha)
+    st = O.OracleSmoother(osys, "lsgs")
+    rng = np.random.default_rng(0)
+    x = rng.uniform(-1, 1, osys.n)
+    r = osys.residual(x, rng.uniform(-1, 1, osys.n))
+    st.lsgs(x, r, True)                      # warm caches
+    t0 = time.perf_counter()
+    for _ in range(sweeps):
+        st.lsgs(x, r, True)
+    dt = (time.perf_counter() - t0) / sweeps
+    return osys.n / dt, dt, osys.n
+
+
+def run_reference_arm(args, ws, rank):
+    if rank != 0:
+        return
+    level = args.cpu_level
+    import oracle as O
+    osys = O.poisson_system(level, args.alpha)
+    st = O.OracleSmoother(osys, "lsgs")
+    rng = np.random.default_rng(0)
+    x = rng.uniform(-1, 1, osys.n)
+    r = osys.residual(x, rng.uniform(-1, 1, osys.n))
+    for _ in range(args.warmup):
+        st.lsgs(x, r, True)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        st.lsgs(x, r, True)
+    dt = (time.perf_counter() - t0) / args.steps
+    v = osys.n / dt
+    out = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded U[-1,1])",
+        "config": {"workload": f"poisson_control_L{args.level}_ne_gs_sweep",
+                   "sample": f"L{level} sweep", "alpha": args.alpha},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": f"forward NE-GS sweep of Poisson control "
+                                   f"L{level} ({osys.n} unknowns) x "
+                                   f"{args.steps}, oracle C port of "
+                                   "kernels.lsgs_sweep, 1 thread"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def time_events(fn, iters, stream):
+    import torch
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    start.record(stream)
+    for _ in range(iters):
+        fn()
+    stop.record(stream)
+    stop.synchronize()
+    return start.elapsed_time(stop) / iters / 1e3
+
+
+def kernel_table(dsys, coarse_sys, transfer, x, r, f, stream, iters, hbm):
+    """Each hot kernel of a cycle on the finest level, CUDA-event timed."""
+    import paper_1502_03917_b200 as P
+    n = dsys.n
+    rows = {}
+    gs = P.make_smoother(dsys, "lsgs", gs_mode="wavefront")
+    mc = P.make_smoother(dsys, "lsgs", gs_mode="multicolour")
+    nj = P.make_smoother(dsys, "normal")
+    res_out = r.clone()
+    import torch
+    rc = torch.empty(coarse_sys.n, dtype=torch.float64, device=x.device)
+
+    def add(name, key, t, units):
+        rows[name] = {"dof_per_s": units / t, "ms": t * 1e3,
+                      "gbs": BYTES[key] * units / t / 1e9,
+                      "frac_hbm": BYTES[key] * units / t / 1e9 / hbm}
+    from paper_1502_03917_b200 import _lib
+    add("residual", "residual", time_events(
+        lambda: _lib.call("ocmg_residual", dsys.handle, _lib.dptr(x),
+                          _lib.dptr(f), _lib.dptr(res_out),
+                          _lib.stream_ptr()), iters, stream), n)
+    add("ne_jacobi", "ne_jacobi",
+        time_events(lambda: nj.sweep(x, r), iters, stream), n)
+    add("ne_gs_wavefront", "ne_gs",
+        time_events(lambda: gs.sweep(x, r), iters, stream), n)
+    add("ne_gs_multicolour", "ne_gs",
+        time_events(lambda: mc.sweep(x, r), iters, stream), n)
+    add("restrict", "restrict", time_events(
+        lambda: transfer.restrict(r, rc), iters, stream), n)
+    add("prolong_add", "prolong", time_events(
+        lambda: transfer.prolong_add(rc, x), iters, stream), n)
+    return rows
+
+
+def solve_timing(level, alpha, cycle, coarsest, mode, sine):
+    """Time to 1e-8 relative residual (BASELINE protocol), setup excluded."""
+    import torch
+
+    import paper_1502_03917_b200 as P
+    t_setup = time.perf_counter()
+    cfg = P.CycleConfig(smoother=P.SmootherKind("lsgs"), cycle=cycle,
+                        coarsest_level=coarsest, gs_mode=mode)
+    mg = P.build_solver("poisson", level, alpha, cfg)
+    f = P.baseline_rhs(mg.finest, 0, add_sine=sine)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t_setup
+    mg.solve_to_tolerance(f, tol=1e-8, max_cycles=2)      # graph capture
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _, hist = mg.solve_to_tolerance(f, tol=1e-8, max_cycles=300)
+    torch.cuda.synchronize()
+    t = time.perf_counter() - t0
+    return {"config": f"poisson L{level} alpha={alpha} {cycle.upper()}(2,2) "
+                      f"NE-GS[{mode}] coarsest L{coarsest}"
+                      + (" y_D=U+sin*sin" if sine else ""),
+            "cycles": len(hist), "final_rel_residual": hist[-1],
+            "seconds": t, "setup_seconds": t_setup}
+
+
+def run_gpu_arm(args, ws, rank, local):
+    import torch
+
+    import paper_1502_03917_b200 as P
+    from paper_1502_03917_b200 import _lib
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    hbm, peak_kind = peaks()
+
+    dsys = P.build_poisson_system(args.level, args.alpha)
+    n = dsys.n
+    g = torch.Generator(device=device).manual_seed(1234 + rank)
+    x = torch.rand(n, dtype=torch.float64, device=device, generator=g) * 2 - 1
+    f = torch.rand(n, dtype=torch.float64, device=device, generator=g) * 2 - 1
+    r = dsys.residual(x, f)
+    st = P.make_smoother(dsys, "lsgs", gs_mode=args.mode)
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        st.sweep(x, r)
+    torch.cuda.synchronize()
+    barrier(ws)
+
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        time.sleep(0.3)
+        launches0 = _lib.launch_count()
+        barrier(ws)
+        torch.cuda.synchronize()
+        start.record(stream)
+        for _ in range(args.steps):
+            st.sweep(x, r)
+        stop.record(stream)
+        stop.synchronize()
+        launches = _lib.launch_count() - launches0
+        barrier(ws)
+    t_step = start.elapsed_time(stop) / args.steps / 1e3
+    t_step = max_over_ranks(t_step, ws, device)
+    value = ws * n / t_step
+
+    # end to end through the public API with host buffers (pinned)
+    xh = x.cpu().pin_memory()
+    rh = r.cpu().pin_memory()
+    xd, rd = torch.empty_like(x), torch.empty_like(r)
+
+    def e2e_step():
+        xd.copy_(xh, non_blocking=True)
+        rd.copy_(rh, non_blocking=True)
+        st.sweep(xd, rd)
+        xh.copy_(xd, non_blocking=True)
+        rh.copy_(rd, non_blocking=True)
+    e2e_step()
+    t_e2e = time_events(e2e_step, max(1, args.steps), stream)
+    t_e2e = max_over_ranks(t_e2e, ws, device)
+
+    result = None
+    if rank == 0:
+        achieved = BYTES["ne_gs"] * n / t_step / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            tr = json.load(open(tp))
+            traffic = tr.get(f"ne_gs_{args.mode}_L{args.level}")
+        result = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_step * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded U[-1,1] iterate and rhs)",
+            "config": {"workload": f"poisson_control_L{args.level}_ne_gs_sweep",
+                       "unknowns": n, "alpha": args.alpha,
+                       "gs_mode": args.mode,
+                       "l2": "inputs larger than L2 (x+r 2x268 MB), no flush",
+                       "parallelism": f"replicas x{ws}"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm,
+                         "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic,
+                         "bytes_per_dof": BYTES["ne_gs"]},
+            "e2e": {"value": ws * n / t_e2e, "unit": UNIT,
+                    "h2d_bytes_per_step": 2 * 8 * n,
+                    "d2h_bytes_per_step": 2 * 8 * n},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        if not args.quick:
+            from paper_1502_03917_b200.transfer import system_transfer
+            coarse = P.build_poisson_system(args.level - 1, args.alpha)
+            tr = system_transfer(coarse, dsys)
+            result["kernels"] = kernel_table(dsys, coarse, tr, x, r, f,
+                                             stream, args.kernel_iters, hbm)
+            result["solve"] = [solve_timing(10, 1e-4, "v", 2, args.mode,
+                                            False)]
+            if args.solve_l12:
+                result["solve"].append(solve_timing(
+                    args.level, args.alpha, "w", 1, args.mode, True))
+        if ws == 1 and not args.no_cpu:
+            v, dt, ncpu = cpu_sweep_rate(args.cpu_level, args.cpu_sweeps,
+                                         args.alpha)
+            result["cpu_baseline"] = {
+                "value": v, "unit": UNIT, "cores": 1, "kind": "port",
+                "sample": f"forward NE-GS sweep, Poisson control "
+                          f"L{args.cpu_level} ({ncpu} unknowns) x "
+                          f"{args.cpu_sweeps}, oracle C port of "
+                          f"kernels.lsgs_sweep, 1 of {os.cpu_count()} host "
+                          "threads"}
+        print(json.dumps(result), flush=True)
+    barrier(ws)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--level", type=int, default=12)
+    ap.add_argument("--alpha", type=float, default=1e-6)
+    ap.add_argument("--mode", default="wavefront",
+                    choices=["wavefront", "reference", "multicolour"])
+    ap.add_argument("--quick", action="store_true",
+                    help="headline only (no kernel table / solves)")
+    ap.add_argument("--solve-l12", action="store_true",
+                    help="also time the config-3 W-cycle solve at L12")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-level", type=int, default=10)
+    ap.add_argument("--cpu-sweeps", type=int, default=10)
+    ap.add_argument("--kernel-iters", type=int, default=5)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup raised to 3 (timing rules)", file=sys.stderr)
+        args.warmup = 3
+    ws, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference_arm(args, ws, rank)
+    else:
+        run_gpu_arm(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,837 @@
+// C ABI of the ocmg_b200 library (declared in include/ocmg_b200.h).
+//
+// Owns the per-level device data (what SmootherState.__init__ precomputes,
+// smoothers.py:189-216), the transfers (transfer.py), the coarse LU
+// (multigrid.py:67-102) and the on-device cycle driver (multigrid.py:130-204),
+// and dispatches to the kernels in ocmg_csr.cuh / ocmg_p1.cuh /
+// ocmg_wavefront.cuh.
+#include <algorithm>
+#include <cmath>
+#include <memory>
+
+#include "ocmg_common.cuh"
+#include "ocmg_csr.cuh"
+#include "ocmg_p1.cuh"
+#include "ocmg_wavefront.cuh"
+
+using namespace ocmg;
+
+namespace {
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F &&fn) {
+    try {
+        fn();
+        return OCMG_OK;
+    } catch (const Error &e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::exception &e) {
+        g_last_error = e.what();
+        return OCMG_E_STATE;
+    }
+}
+
+enum LevelKind { kCsr = 0, kP1 = 1 };
+
+struct Schedule {  // rows bucketed by dependency level (or colour)
+    DevBuf<int32_t> rows;
+    std::vector<int64_t> off;
+};
+
+}  // namespace
+
+struct ocmg_level {
+    int problem = OCMG_POISSON;
+    int kind = kCsr;
+    int64_t n = 0, nnz = 0;
+    std::vector<int64_t> field_off;
+    uint32_t pmask = 0;
+    // generic CSR
+    CsrDev A;
+    DevBuf<double> W, L, ndiag;
+    Schedule sched[2];  // 0 forward, 1 backward
+    Schedule colours;
+    bool has_colours = false;
+    // structured P1
+    int k = 0, n1 = 0;
+    double alpha = 0.0;
+    DevBuf<double> tables;
+    P1Wavefront wf;
+    // reduction scratch
+    DevBuf<double> partial, scal;
+};
+
+struct ocmg_transfer {
+    int kind = kCsr;
+    int64_t nf = 0, nc = 0;
+    CsrDev P, R;
+    int kc = 0, nc1 = 0, n_fields = 0;
+};
+
+struct ocmg_coarse {
+    int problem = OCMG_POISSON;
+    int64_t n = 0, p_off = 0, mu_off = 0, n_p = 0;
+    DevBuf<double> lu;
+    DevBuf<int32_t> piv;
+};
+
+struct ocmg_hierarchy {
+    std::vector<ocmg_level *> levels;  // index 0 = hierarchy index 1
+    std::vector<ocmg_transfer *> transfers;
+    ocmg_coarse *coarse = nullptr;
+    ocmg_cycle_config cfg{};
+    // per hierarchy index h (0 = coarse): residual r[h] and NE scratch for
+    // h>=1, and for h < top: restricted rhs crhs[h], correction corr[h]
+    std::vector<DevBuf<double>> r, scratch, crhs, corr;
+    DevBuf<double> tmp, scal;
+    cudaGraphExec_t graph = nullptr;
+    const double *graph_x = nullptr, *graph_f = nullptr;
+    cudaStream_t graph_stream = nullptr;
+    ~ocmg_hierarchy() {
+        if (graph) cudaGraphExecDestroy(graph);
+    }
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// host-side setup helpers
+// ---------------------------------------------------------------------------
+
+// ASAP dependency levels of the sequential NE-GS sweep: unknown i touches
+// (reads and writes) r_j for every j in column i = row i; it must follow
+// every earlier unknown touching one of those j.
+Schedule build_schedule(int64_t n, const int64_t *off, const int64_t *col,
+                        bool forward) {
+    std::vector<int32_t> lev(n), touch(n, -1);
+    int32_t maxlev = -1;
+    for (int64_t s = 0; s < n; ++s) {
+        const int64_t i = forward ? s : n - 1 - s;
+        int32_t m = -1;
+        for (int64_t t = off[i]; t < off[i + 1]; ++t)
+            m = std::max(m, touch[col[t]]);
+        lev[i] = m + 1;
+        for (int64_t t = off[i]; t < off[i + 1]; ++t) touch[col[t]] = m + 1;
+        maxlev = std::max(maxlev, m + 1);
+    }
+    Schedule S;
+    S.off.assign(maxlev + 2, 0);
+    for (int64_t i = 0; i < n; ++i) S.off[lev[i] + 1]++;
+    for (size_t l = 1; l < S.off.size(); ++l) S.off[l] += S.off[l - 1];
+    std::vector<int32_t> rows(n);
+    std::vector<int64_t> fill(S.off.begin(), S.off.end() - 1);
+    for (int64_t s = 0; s < n; ++s) {
+        const int64_t i = forward ? s : n - 1 - s;
+        rows[fill[lev[i]]++] = (int32_t)i;
+    }
+    S.rows.upload(rows);
+    return S;
+}
+
+// Greedy distance-2 colouring in index order (smallest free colour).
+Schedule build_colouring(int64_t n, const int64_t *off, const int64_t *col) {
+    std::vector<int32_t> colour(n, -1), mark;
+    int32_t ncol = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        for (int64_t t = off[i]; t < off[i + 1]; ++t) {
+            const int64_t j = col[t];
+            for (int64_t u = off[j]; u < off[j + 1]; ++u) {
+                const int32_t c = colour[col[u]];
+                if (c >= 0) {
+                    if ((int32_t)mark.size() <= c) mark.resize(c + 1, -1);
+                    mark[c] = (int32_t)i;
+                }
+            }
+        }
+        int32_t c = 0;
+        while (c < (int32_t)mark.size() && mark[c] == (int32_t)i) ++c;
+        colour[i] = c;
+        ncol = std::max(ncol, c + 1);
+    }
+    Schedule S;
+    S.off.assign(ncol + 1, 0);
+    for (int64_t i = 0; i < n; ++i) S.off[colour[i] + 1]++;
+    for (int c = 1; c <= ncol; ++c) S.off[c] += S.off[c - 1];
+    std::vector<int32_t> rows(n);
+    std::vector<int64_t> fill(S.off.begin(), S.off.end() - 1);
+    for (int64_t i = 0; i < n; ++i) rows[fill[colour[i]]++] = (int32_t)i;
+    S.rows.upload(rows);
+    return S;
+}
+
+void upload_csr(CsrDev &C, int64_t nrows, int64_t ncols, const int64_t *off,
+                const int64_t *col, const double *val) {
+    C.n = nrows;
+    C.ncols = ncols;
+    C.nnz = off[nrows];
+    C.off.upload(off, nrows + 1);
+    std::vector<int32_t> c32(C.nnz);
+    for (int64_t t = 0; t < C.nnz; ++t) {
+        OCMG_REQUIRE(col[t] >= 0 && col[t] < ncols, "column index out of range");
+        c32[t] = (int32_t)col[t];
+    }
+    C.col.upload(c32);
+    C.val.upload(val, C.nnz);
+}
+
+void csr_transpose(int64_t nrows, int64_t ncols, const int64_t *off,
+                   const int64_t *col, const double *val,
+                   std::vector<int64_t> &toff, std::vector<int64_t> &tcol,
+                   std::vector<double> &tval) {
+    const int64_t nnz = off[nrows];
+    toff.assign(ncols + 1, 0);
+    for (int64_t t = 0; t < nnz; ++t) toff[col[t] + 1]++;
+    for (int64_t c = 0; c < ncols; ++c) toff[c + 1] += toff[c];
+    tcol.resize(nnz);
+    tval.resize(nnz);
+    std::vector<int64_t> fill(toff.begin(), toff.end() - 1);
+    for (int64_t i = 0; i < nrows; ++i)
+        for (int64_t t = off[i]; t < off[i + 1]; ++t) {
+            const int64_t p = fill[col[t]]++;
+            tcol[p] = i;
+            tval[p] = val[t];
+        }
+}
+
+// ---------------------------------------------------------------------------
+// level operations
+// ---------------------------------------------------------------------------
+
+constexpr int kBlk = 256;
+
+void level_residual(const ocmg_level *lv, const double *x, const double *f,
+                    double *r, cudaStream_t s) {
+    if (lv->kind == kP1) {
+        OCMG_LAUNCH(k_p1_residual, grid_for((int64_t)lv->n1 * lv->n1, kBlk), kBlk, 0, s, 
+            lv->n1, lv->tables.p, x, f, r);
+    } else {
+        OCMG_LAUNCH(k_csr_residual, grid_for(lv->n, kBlk), kBlk, 0, s, 
+            lv->n, lv->A.off.p, lv->A.col.p, lv->A.val.p, x, f, r);
+    }
+    OCMG_LAUNCH_CHECK();
+}
+
+void level_ne_jacobi(const ocmg_level *lv, double tau, double *x, double *r,
+                     double *scratch, cudaStream_t s) {
+    if (lv->kind == kP1) {
+        const int64_t N = (int64_t)lv->n1 * lv->n1;
+        OCMG_LAUNCH(k_p1_ne_p, grid_for(N, kBlk), kBlk, 0, s, lv->n1, lv->tables.p, tau,
+                                                     r, scratch);
+        OCMG_LAUNCH(k_p1_ne_apply, grid_for(N, kBlk), kBlk, 0, s, lv->n1, lv->tables.p,
+                                                         scratch, x, r);
+    } else {
+        OCMG_LAUNCH(k_csr_ne_p, grid_for(lv->n, kBlk), kBlk, 0, s, 
+            lv->n, lv->A.off.p, lv->A.col.p, lv->W.p, lv->L.p, tau, r, scratch);
+        OCMG_LAUNCH(k_csr_ne_apply, grid_for(lv->n, kBlk), kBlk, 0, s, 
+            lv->n, lv->A.off.p, lv->A.col.p, lv->A.val.p, scratch, x, r);
+    }
+    OCMG_LAUNCH_CHECK();
+}
+
+void run_schedule(const ocmg_level *lv, const Schedule &S, bool reverse,
+                  double *x, double *r, cudaStream_t s) {
+    const int64_t nb = (int64_t)S.off.size() - 1;
+    for (int64_t b = 0; b < nb; ++b) {
+        const int64_t l = reverse ? nb - 1 - b : b;
+        const int64_t lo = S.off[l], cnt = S.off[l + 1] - lo;
+        if (!cnt) continue;
+        const int blk = cnt < 128 ? 32 * (int)((cnt + 31) / 32) : 128;
+        OCMG_LAUNCH(k_csr_gs_rows, grid_for(cnt, blk), blk, 0, s, 
+            (int)cnt, S.rows.p + lo, lv->A.off.p, lv->A.col.p, lv->A.val.p,
+            lv->W.p, lv->ndiag.p, x, r);
+    }
+    OCMG_LAUNCH_CHECK();
+}
+
+void level_ne_gs(const ocmg_level *lv, int mode, bool forward, double *x,
+                 double *r, cudaStream_t s) {
+    OCMG_REQUIRE(mode >= OCMG_GS_REFERENCE && mode <= OCMG_GS_MULTICOLOUR,
+                 "unknown NE-GS mode");
+    if (lv->kind == kP1) {
+        const int n1 = lv->n1;
+        if (mode == OCMG_GS_MULTICOLOUR) {
+            const int64_t work = (int64_t)((n1 + 6) / 7) * n1;
+            for (int b = 0; b < 14; ++b) {
+                const int c = forward ? b : 13 - b;
+                OCMG_LAUNCH(k_p1_gs_colour, grid_for(work, kBlk), kBlk, 0, s, 
+                    n1, lv->tables.p, c, x, r);
+            }
+        } else if (mode == OCMG_GS_WAVEFRONT && lv->wf.ready()) {
+            lv->wf.sweep(forward, x, r, s);
+        } else {
+            const int depth = 3 * (n1 - 1) + 8;
+            const int blk = 2 * n1 < 256 ? 32 * ((2 * n1 + 31) / 32) : 256;
+            for (int t = 0; t < depth; ++t)
+                OCMG_LAUNCH(k_p1_gs_level, grid_for(2 * n1, blk), blk, 0, s, 
+                    n1, lv->tables.p, t, forward ? 1 : 0, x, r);
+        }
+        OCMG_LAUNCH_CHECK();
+        return;
+    }
+    if (mode == OCMG_GS_MULTICOLOUR) {
+        OCMG_REQUIRE(lv->has_colours,
+                     "multicolour NE-GS needs a level created with colouring");
+        run_schedule(lv, lv->colours, !forward, x, r, s);
+    } else {
+        run_schedule(lv, lv->sched[forward ? 0 : 1], false, x, r, s);
+    }
+}
+
+void level_mean_project(const ocmg_level *lv, double *x, cudaStream_t s) {
+    if (lv->problem != OCMG_STOKES) return;
+    const int nf = (int)lv->field_off.size() - 1;
+    for (int f = 0; f < nf; ++f) {
+        if (!((lv->pmask >> f) & 1u)) continue;
+        const int64_t lo = lv->field_off[f], hi = lv->field_off[f + 1];
+        OCMG_LAUNCH(k_sum_partial, kRedGrid, kRedBlock, 0, s, lo, hi, x, lv->partial.p);
+        OCMG_LAUNCH(k_finish_sum, 1, kRedBlock, 0, s, kRedGrid, lv->partial.p,
+                                             (double)(hi - lo), lv->scal.p + f);
+        OCMG_LAUNCH(k_sub_scalar, grid_for(hi - lo, kBlk), kBlk, 0, s, lo, hi, x,
+                                                              lv->scal.p + f);
+    }
+    OCMG_LAUNCH_CHECK();
+}
+
+void sumsq(int64_t n, const double *x, const double *w, double *partial,
+           double *out, cudaStream_t s) {
+    OCMG_LAUNCH(k_sumsq_partial, kRedGrid, kRedBlock, 0, s, n, x, w, partial);
+    OCMG_LAUNCH(k_finish_sum, 1, kRedBlock, 0, s, kRedGrid, partial, 1.0, out);
+    OCMG_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
+// coarse solve: pivoted LU substitution in one CTA
+// ---------------------------------------------------------------------------
+__global__ void k_coarse_solve(int n, const double *__restrict__ lu,
+                               const int32_t *__restrict__ piv, int stokes,
+                               int p_off, int mu_off, int n_p,
+                               const double *__restrict__ rhs,
+                               double *__restrict__ xout) {
+    extern __shared__ double b[];
+    __shared__ double sh[32];
+    __shared__ double mean[2];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) b[i] = rhs[i];
+    __syncthreads();
+    const int offs[2] = {p_off, mu_off};
+    if (stokes) {  // project the rhs, pin (multigrid.py:95-99)
+        for (int f = 0; f < 2; ++f) {
+            double acc = 0.0;
+            for (int i = threadIdx.x; i < n_p; i += blockDim.x)
+                acc += b[offs[f] + i];
+            acc = block_sum(acc, sh);
+            if (threadIdx.x == 0) mean[f] = acc / (double)n_p;
+            __syncthreads();
+            for (int i = threadIdx.x; i < n_p; i += blockDim.x)
+                b[offs[f] + i] -= mean[f];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            b[p_off] = 0.0;
+            b[mu_off] = 0.0;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)  // row interchanges (getrs / laswp)
+        for (int i = 0; i < n; ++i) {
+            const int p = piv[i];
+            if (p != i) {
+                const double t = b[i];
+                b[i] = b[p];
+                b[p] = t;
+            }
+        }
+    __syncthreads();
+    for (int j = 0; j < n; ++j) {  // unit lower solve, column oriented
+        const double bj = b[j];
+        for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x)
+            b[i] -= lu[i + (int64_t)j * n] * bj;
+        __syncthreads();
+    }
+    for (int j = n - 1; j >= 0; --j) {  // upper solve
+        if (threadIdx.x == 0) b[j] /= lu[j + (int64_t)j * n];
+        __syncthreads();
+        const double bj = b[j];
+        for (int i = threadIdx.x; i < j; i += blockDim.x)
+            b[i] -= lu[i + (int64_t)j * n] * bj;
+        __syncthreads();
+    }
+    if (stokes) {  // re-centre (pressure_mean_projection)
+        for (int f = 0; f < 2; ++f) {
+            double acc = 0.0;
+            for (int i = threadIdx.x; i < n_p; i += blockDim.x)
+                acc += b[offs[f] + i];
+            acc = block_sum(acc, sh);
+            if (threadIdx.x == 0) mean[f] = acc / (double)n_p;
+            __syncthreads();
+            for (int i = threadIdx.x; i < n_p; i += blockDim.x)
+                b[offs[f] + i] -= mean[f];
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) xout[i] = b[i];
+}
+
+void coarse_solve(const ocmg_coarse *c, const double *rhs, double *x,
+                  cudaStream_t s) {
+    const size_t smem = (size_t)c->n * sizeof(double);
+    OCMG_LAUNCH(k_coarse_solve, 1, 256, smem, s, 
+        (int)c->n, c->lu.p, c->piv.p, c->problem == OCMG_STOKES ? 1 : 0,
+        (int)c->p_off, (int)c->mu_off, (int)c->n_p, rhs, x);
+    OCMG_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
+// transfers
+// ---------------------------------------------------------------------------
+void do_restrict(const ocmg_transfer *t, const double *rf, double *rc,
+                 cudaStream_t s) {
+    if (t->kind == kP1) {
+        OCMG_LAUNCH(k_p1_restrict, grid_for((int64_t)t->nc1 * t->nc1, kBlk), kBlk, 0, s, 
+            t->nc1, t->n_fields, rf, rc);
+    } else {
+        OCMG_LAUNCH(k_csr_spmv, grid_for(t->nc, kBlk), kBlk, 0, s, 
+            t->nc, t->R.off.p, t->R.col.p, t->R.val.p, rf, rc);
+    }
+    OCMG_LAUNCH_CHECK();
+}
+
+void do_prolong_add(const ocmg_transfer *t, const double *c, double *xf,
+                    cudaStream_t s) {
+    if (t->kind == kP1) {
+        const int nf1 = 2 * t->nc1 - 1;
+        OCMG_LAUNCH(k_p1_prolong_add, grid_for((int64_t)nf1 * nf1, kBlk), kBlk, 0, s, 
+            t->nc1, t->n_fields, c, xf);
+    } else {
+        OCMG_LAUNCH(k_csr_spmv_add, grid_for(t->nf, kBlk), kBlk, 0, s, 
+            t->nf, t->P.off.p, t->P.col.p, t->P.val.p, c, xf);
+    }
+    OCMG_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
+// cycle driver (multigrid.py:130-159)
+// ---------------------------------------------------------------------------
+void smooth(ocmg_hierarchy *h, int hi, double *x, double *r, cudaStream_t s) {
+    ocmg_level *lv = h->levels[hi - 1];
+    const ocmg_cycle_config &c = h->cfg;
+    switch (c.smoother) {
+    case OCMG_SMOOTHER_NORMAL:
+        level_ne_jacobi(lv, c.tau, x, r, h->scratch[hi].p, s);
+        break;
+    case OCMG_SMOOTHER_LSGS:
+        level_ne_gs(lv, c.gs_mode, true, x, r, s);
+        break;
+    default:
+        level_ne_gs(lv, c.gs_mode, true, x, r, s);
+        level_ne_gs(lv, c.gs_mode, false, x, r, s);
+    }
+}
+
+void cycle_rec(ocmg_hierarchy *h, int hi, double *x, const double *rhs,
+               cudaStream_t s) {
+    if (hi == 0) {
+        coarse_solve(h->coarse, rhs, x, s);
+        return;
+    }
+    ocmg_level *lv = h->levels[hi - 1];
+    ocmg_transfer *tr = h->transfers[hi - 1];
+    double *r = h->r[hi].p;
+    level_residual(lv, x, rhs, r, s);
+    for (int i = 0; i < h->cfg.nu_pre; ++i) smooth(h, hi, x, r, s);
+    double *crhs = h->crhs[hi - 1].p, *corr = h->corr[hi - 1].p;
+    do_restrict(tr, r, crhs, s);
+    const int64_t nc = h->corr[hi - 1].n;
+    OCMG_CUDA(cudaMemsetAsync(corr, 0, nc * sizeof(double), s));
+    // the exact coarse solve ignores its start vector, so the W-cycle's
+    // second visit of level 0 would recompute the same vector: elided
+    const int rec = (h->cfg.cycle_w && hi - 1 > 0) ? 2 : 1;
+    for (int k = 0; k < rec; ++k) cycle_rec(h, hi - 1, corr, crhs, s);
+    do_prolong_add(tr, corr, x, s);
+    level_mean_project(lv, x, s);
+    level_residual(lv, x, rhs, r, s);
+    for (int i = 0; i < h->cfg.nu_post; ++i) smooth(h, hi, x, r, s);
+}
+
+// one cycle + projection + ||f - A x||^2 into h->scal[0]
+void cycle_and_measure(ocmg_hierarchy *h, double *x, const double *f,
+                       cudaStream_t s) {
+    const int top = (int)h->levels.size();
+    cycle_rec(h, top, x, f, s);
+    ocmg_level *fine = h->levels.back();
+    level_mean_project(fine, x, s);
+    level_residual(fine, x, f, h->tmp.p, s);
+    sumsq(fine->n, h->tmp.p, nullptr, fine->partial.p, h->scal.p, s);
+}
+
+}  // namespace
+
+// ===========================================================================
+// extern "C"
+// ===========================================================================
+extern "C" {
+
+const char *ocmg_last_error(void) { return g_last_error.c_str(); }
+int ocmg_abi_version(void) { return 1; }
+
+int ocmg_device_sm_count(int *out) {
+    return guarded([&] {
+        int dev = 0;
+        OCMG_CUDA(cudaGetDevice(&dev));
+        OCMG_CUDA(cudaDeviceGetAttribute(out, cudaDevAttrMultiProcessorCount, dev));
+    });
+}
+
+int ocmg_launch_count(int64_t *out) {
+    return guarded([&] {
+        OCMG_REQUIRE(out, "null argument");
+        *out = launch_counter().load();
+    });
+}
+
+int ocmg_level_create_csr(int problem, int64_t n, const int64_t *row_off,
+                          const int64_t *col, const double *val,
+                          const double *norm_diag, int n_fields,
+                          const int64_t *field_off, uint32_t pressure_mask,
+                          int want_colouring, ocmg_level **out) {
+    return guarded([&] {
+        OCMG_REQUIRE(out && row_off && col && val && norm_diag,
+                     "null argument");
+        OCMG_REQUIRE(n > 0 && n < (int64_t)1 << 31, "bad level size");
+        OCMG_REQUIRE(n_fields >= 1 && field_off && field_off[0] == 0 &&
+                         field_off[n_fields] == n,
+                     "field offsets do not cover the level");
+        for (int64_t i = 0; i < n; ++i)
+            OCMG_REQUIRE(norm_diag[i] > 0.0, "norm_diag must be positive");
+        // symmetric (bitwise) operator: column i == row i
+        {
+            std::vector<int64_t> toff, tcol;
+            std::vector<double> tval;
+            csr_transpose(n, n, row_off, col, val, toff, tcol, tval);
+            for (int64_t i = 0; i <= n; ++i)
+                OCMG_REQUIRE(toff[i] == row_off[i], "operator is not symmetric");
+            for (int64_t t = 0; t < row_off[n]; ++t)
+                OCMG_REQUIRE(tcol[t] == col[t] && tval[t] == val[t],
+                             "operator is not symmetric");
+        }
+        auto lv = std::make_unique<ocmg_level>();
+        lv->problem = problem;
+        lv->kind = kCsr;
+        lv->n = n;
+        lv->field_off.assign(field_off, field_off + n_fields + 1);
+        lv->pmask = pressure_mask;
+        upload_csr(lv->A, n, n, row_off, col, val);
+        lv->nnz = lv->A.nnz;
+        lv->L.upload(norm_diag, n);
+        lv->W.alloc(lv->nnz);
+        lv->ndiag.alloc(n);
+        OCMG_LAUNCH(k_csr_row_scaled, grid_for(lv->nnz, kBlk), kBlk, 0, 0, 
+            lv->nnz, lv->A.col.p, lv->A.val.p, lv->L.p, lv->W.p);
+        OCMG_LAUNCH(k_csr_ndiag, grid_for(n, kBlk), kBlk, 0, 0, n, lv->A.off.p,
+                    lv->A.val.p, lv->W.p, lv->ndiag.p);
+        OCMG_LAUNCH_CHECK();
+        lv->sched[0] = build_schedule(n, row_off, col, true);
+        lv->sched[1] = build_schedule(n, row_off, col, false);
+        if (want_colouring) {
+            lv->colours = build_colouring(n, row_off, col);
+            lv->has_colours = true;
+        }
+        lv->partial.alloc(kRedGrid);
+        lv->scal.alloc(8);
+        // n_diag > 0 check (smoothers.py:213-215)
+        std::vector<double> nd(n);
+        OCMG_CUDA(cudaMemcpy(nd.data(), lv->ndiag.p, n * sizeof(double),
+                             cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < n; ++i)
+            OCMG_REQUIRE(nd[i] > 0.0, "operator has an empty row; the "
+                                      "normal-equation diagonal degenerates");
+        *out = lv.release();
+    });
+}
+
+int ocmg_level_create_p1(int k, double alpha, const double *tables,
+                         int64_t n_tables, ocmg_level **out) {
+    return guarded([&] {
+        OCMG_REQUIRE(out && tables, "null argument");
+        OCMG_REQUIRE(k >= 3 && k <= 14, "structured P1 levels need 3 <= k <= 14");
+        OCMG_REQUIRE(n_tables == kP1TableDoubles + kWfTableDoubles,
+                     "P1 table size mismatch");
+        OCMG_REQUIRE(alpha > 0.0, "alpha must be positive");
+        auto lv = std::make_unique<ocmg_level>();
+        lv->problem = OCMG_POISSON;
+        lv->kind = kP1;
+        lv->k = k;
+        lv->n1 = (1 << k) + 1;
+        lv->alpha = alpha;
+        const int64_t N = (int64_t)lv->n1 * lv->n1;
+        lv->n = 2 * N;
+        const int64_t pairs = 7 * N - 8 * (int64_t)lv->n1 + 2;
+        lv->nnz = 4 * pairs;
+        lv->field_off = {0, N, 2 * N};
+        lv->tables.upload(tables, n_tables);
+        lv->wf.init(lv->k, lv->n1, lv->tables.p + kP1TableDoubles);
+        lv->partial.alloc(kRedGrid);
+        lv->scal.alloc(8);
+        *out = lv.release();
+    });
+}
+
+int ocmg_level_destroy(ocmg_level *lv) {
+    return guarded([&] { delete lv; });
+}
+
+int64_t ocmg_level_n(const ocmg_level *lv) { return lv ? lv->n : -1; }
+int64_t ocmg_level_nnz(const ocmg_level *lv) { return lv ? lv->nnz : -1; }
+
+int ocmg_residual(const ocmg_level *lv, const double *x, const double *f,
+                  double *r, void *stream) {
+    return guarded([&] {
+        OCMG_REQUIRE(lv && x && r, "null argument");
+        level_residual(lv, x, f, r, as_stream(stream));
+    });
+}
+
+int ocmg_ne_jacobi_sweep(const ocmg_level *lv, double tau, double *x,
+                         double *r, double *scratch, void *stream,
+                         int64_t *ops) {
+    return guarded([&] {
+        OCMG_REQUIRE(lv && x && r && scratch, "null argument");
+        OCMG_REQUIRE(tau > 0.0 && tau < 2.0, "damping parameter must lie in (0, 2)");
+        level_ne_jacobi(lv, tau, x, r, scratch, as_stream(stream));
+        if (ops) *ops = 2 * lv->nnz;
+    });
+}
+
+int ocmg_ne_gs_sweep(const ocmg_level *lv, int mode, int forward, double *x,
+                     double *r, void *stream, int64_t *ops) {
+    return guarded([&] {
+        OCMG_REQUIRE(lv && x && r, "null argument");
+        level_ne_gs(lv, mode, forward != 0, x, r, as_stream(stream));
+        if (ops) *ops = 2 * lv->nnz;
+    });
+}
+
+int ocmg_mean_project(const ocmg_level *lv, double *x, void *stream) {
+    return guarded([&] {
+        OCMG_REQUIRE(lv && x, "null argument");
+        level_mean_project(lv, x, as_stream(stream));
+    });
+}
+
+int ocmg_norm2(const ocmg_level *lv, const double *x, int weighted,
+               double *out_dev, void *stream) {
+    return guarded([&] {
+        OCMG_REQUIRE(lv && x && out_dev, "null argument");
+        cudaStream_t s = as_stream(stream);
+        if (weighted && lv->kind == kP1) {
+            OCMG_LAUNCH(k_p1_wsumsq_partial, kRedGrid, kRedBlock, 0, s, 
+                lv->n1, lv->tables.p, x, lv->partial.p);
+            OCMG_LAUNCH(k_finish_sum, 1, kRedBlock, 0, s, kRedGrid, lv->partial.p, 1.0,
+                                                 out_dev);
+            OCMG_LAUNCH_CHECK();
+            return;
+        }
+        sumsq(lv->n, x, weighted ? lv->L.p : nullptr, lv->partial.p, out_dev,
+              s);
+    });
+}
+
+int ocmg_transfer_create_csr(int64_t nf, int64_t nc, const int64_t *row_off,
+                             const int64_t *col, const double *val,
+                             ocmg_transfer **out) {
+    return guarded([&] {
+        OCMG_REQUIRE(out && row_off && col && val, "null argument");
+        auto t = std::make_unique<ocmg_transfer>();
+        t->kind = kCsr;
+        t->nf = nf;
+        t->nc = nc;
+        upload_csr(t->P, nf, nc, row_off, col, val);
+        std::vector<int64_t> toff, tcol;
+        std::vector<double> tval;
+        csr_transpose(nf, nc, row_off, col, val, toff, tcol, tval);
+        upload_csr(t->R, nc, nf, toff.data(), tcol.data(), tval.data());
+        *out = t.release();
+    });
+}
+
+int ocmg_transfer_create_p1(int kc, int n_fields, ocmg_transfer **out) {
+    return guarded([&] {
+        OCMG_REQUIRE(out && kc >= 0 && kc < 14 && n_fields >= 1,
+                     "bad P1 transfer arguments");
+        auto t = std::make_unique<ocmg_transfer>();
+        t->kind = kP1;
+        t->kc = kc;
+        t->nc1 = (1 << kc) + 1;
+        t->n_fields = n_fields;
+        const int64_t nf1 = 2 * (int64_t)t->nc1 - 1;
+        t->nc = (int64_t)n_fields * t->nc1 * t->nc1;
+        t->nf = (int64_t)n_fields * nf1 * nf1;
+        *out = t.release();
+    });
+}
+
+int ocmg_transfer_destroy(ocmg_transfer *t) {
+    return guarded([&] { delete t; });
+}
+
+int ocmg_restrict(const ocmg_transfer *t, const double *rf, double *rc,
+                  void *stream) {
+    return guarded([&] {
+        OCMG_REQUIRE(t && rf && rc, "null argument");
+        do_restrict(t, rf, rc, as_stream(stream));
+    });
+}
+
+int ocmg_prolong_add(const ocmg_transfer *t, const double *c, double *xf,
+                     void *stream) {
+    return guarded([&] {
+        OCMG_REQUIRE(t && c && xf, "null argument");
+        do_prolong_add(t, c, xf, as_stream(stream));
+    });
+}
+
+int ocmg_coarse_create(int problem, int64_t n, const double *lu,
+                       const int64_t *piv, int64_t p_off, int64_t mu_off,
+                       int64_t n_p, ocmg_coarse **out) {
+    return guarded([&] {
+        OCMG_REQUIRE(out && lu && piv, "null argument");
+        OCMG_REQUIRE(n > 0 && n <= 5000,
+                     "coarsest system too large; raise coarsest_level");
+        for (int64_t i = 0; i < n; ++i)
+            if (lu[i + i * n] == 0.0)
+                throw Error(OCMG_E_SINGULAR,
+                            "exactly singular pivot in LU factorization");
+        auto c = std::make_unique<ocmg_coarse>();
+        c->problem = problem;
+        c->n = n;
+        c->p_off = p_off;
+        c->mu_off = mu_off;
+        c->n_p = n_p;
+        c->lu.upload(lu, (size_t)(n * n));
+        std::vector<int32_t> p32(n);
+        for (int64_t i = 0; i < n; ++i) p32[i] = (int32_t)piv[i];
+        c->piv.upload(p32);
+        *out = c.release();
+    });
+}
+
+int ocmg_coarse_destroy(ocmg_coarse *c) {
+    return guarded([&] { delete c; });
+}
+
+int ocmg_coarse_solve(const ocmg_coarse *c, const double *rhs, double *x,
+                      void *stream) {
+    return guarded([&] {
+        OCMG_REQUIRE(c && rhs && x, "null argument");
+        coarse_solve(c, rhs, x, as_stream(stream));
+    });
+}
+
+int ocmg_hierarchy_create(int n_levels, ocmg_level *const *levels,
+                          ocmg_transfer *const *transfers, ocmg_coarse *coarse,
+                          const ocmg_cycle_config *cfg, ocmg_hierarchy **out) {
+    return guarded([&] {
+        OCMG_REQUIRE(out && levels && transfers && coarse && cfg,
+                     "null argument");
+        OCMG_REQUIRE(n_levels >= 1, "need at least one smoothed level");
+        OCMG_REQUIRE(cfg->nu_pre + cfg->nu_post >= 1,
+                     "need at least one smoothing step per cycle");
+        auto h = std::make_unique<ocmg_hierarchy>();
+        h->levels.assign(levels, levels + n_levels);
+        h->transfers.assign(transfers, transfers + n_levels);
+        h->coarse = coarse;
+        h->cfg = *cfg;
+        h->r.resize(n_levels + 1);
+        h->scratch.resize(n_levels + 1);
+        h->crhs.resize(n_levels);
+        h->corr.resize(n_levels);
+        std::vector<int64_t> sizes(n_levels + 1);
+        sizes[0] = coarse->n;
+        for (int i = 0; i < n_levels; ++i) sizes[i + 1] = levels[i]->n;
+        for (int i = 0; i < n_levels; ++i) {
+            OCMG_REQUIRE(transfers[i]->nc == sizes[i] &&
+                             transfers[i]->nf == sizes[i + 1],
+                         "transfer sizes do not match the levels");
+        }
+        for (int hi = 1; hi <= n_levels; ++hi) {
+            h->r[hi].alloc(sizes[hi]);
+            if (cfg->smoother == OCMG_SMOOTHER_NORMAL)
+                h->scratch[hi].alloc(sizes[hi]);
+        }
+        for (int hi = 0; hi < n_levels; ++hi) {
+            h->crhs[hi].alloc(sizes[hi]);
+            h->corr[hi].alloc(sizes[hi]);
+        }
+        h->tmp.alloc(sizes[n_levels]);
+        h->scal.alloc(8);
+        *out = h.release();
+    });
+}
+
+int ocmg_hierarchy_destroy(ocmg_hierarchy *h) {
+    return guarded([&] { delete h; });
+}
+
+int ocmg_cycle(ocmg_hierarchy *h, double *x, const double *f, void *stream) {
+    return guarded([&] {
+        OCMG_REQUIRE(h && x && f, "null argument");
+        cycle_rec(h, (int)h->levels.size(), x, f, as_stream(stream));
+    });
+}
+
+int ocmg_solve(ocmg_hierarchy *h, double *x, const double *f, double tol,
+               int max_cycles, int use_graph, double *hist, int *n_done,
+               void *stream) {
+    return guarded([&] {
+        OCMG_REQUIRE(h && x && f && hist && n_done, "null argument");
+        cudaStream_t s = as_stream(stream);
+        ocmg_level *fine = h->levels.back();
+        // ||f||^2
+        sumsq(fine->n, f, nullptr, fine->partial.p, h->scal.p + 1, s);
+        double fn2 = 0.0;
+        OCMG_CUDA(cudaMemcpyAsync(&fn2, h->scal.p + 1, sizeof(double),
+                                  cudaMemcpyDeviceToHost, s));
+        OCMG_CUDA(cudaStreamSynchronize(s));
+        const double fn = std::sqrt(fn2);
+        OCMG_REQUIRE(fn > 0.0, "right-hand side is zero");
+        const bool graphs = use_graph && s != nullptr;
+        if (graphs && (h->graph_x != x || h->graph_f != f ||
+                       h->graph_stream != s)) {
+            if (h->graph) cudaGraphExecDestroy(h->graph);
+            h->graph = nullptr;
+            cudaGraph_t g;
+            OCMG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            try {
+                cycle_and_measure(h, x, f, s);
+            } catch (...) {
+                cudaStreamEndCapture(s, &g);
+                throw;
+            }
+            OCMG_CUDA(cudaStreamEndCapture(s, &g));
+            OCMG_CUDA(cudaGraphInstantiate(&h->graph, g, 0));
+            cudaGraphDestroy(g);
+            h->graph_x = x;
+            h->graph_f = f;
+            h->graph_stream = s;
+        }
+        int done = 0;
+        for (int c = 0; c < max_cycles; ++c) {
+            if (graphs)
+                OCMG_CUDA(cudaGraphLaunch(h->graph, s));
+            else
+                cycle_and_measure(h, x, f, s);
+            double r2 = 0.0;
+            OCMG_CUDA(cudaMemcpyAsync(&r2, h->scal.p, sizeof(double),
+                                      cudaMemcpyDeviceToHost, s));
+            OCMG_CUDA(cudaStreamSynchronize(s));
+            const double rel = std::sqrt(r2) / fn;
+            hist[c] = rel;
+            done = c + 1;
+            if (rel <= tol || !std::isfinite(rel)) break;
+        }
+        *n_done = done;
+    });
+}
+
+}  // extern "C"

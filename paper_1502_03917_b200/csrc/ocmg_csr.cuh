@@ -1,0 +1,155 @@
+// Generic CSR kernels (any block operator: Stokes Taylor-Hood, Poisson on
+// levels too small for the stencil path).  Every kernel reproduces the
+// reference's per-unknown arithmetic exactly: sums start at 0.0 and run in
+// CSR column order, multiplies and adds round separately (the library is
+// built with --fmad=false; see Makefile), division is IEEE.
+//
+//   k_csr_residual      <- BlockSystem.residual   assembly.py:259-263
+//   k_csr_ne_p          <- normal_sweep phase 1   kernels.py:27-32
+//   k_csr_ne_apply      <- normal_sweep phase 2   kernels.py:33-38 (row gather:
+//                          r_j receives A_ji p_i in increasing i, exactly the
+//                          order of the reference's column scatter)
+//   k_csr_gs_rows       <- lsgs_sweep body        kernels.py:57-64, run over the
+//                          rows of one dependency level (or one colour)
+//   k_csr_spmv(_add)    <- SparseMatrix.matvec    sparse.py:152-158
+#pragma once
+
+#include "ocmg_common.cuh"
+
+namespace ocmg {
+
+struct CsrDev {
+    int64_t n = 0, ncols = 0, nnz = 0;
+    DevBuf<int64_t> off;
+    DevBuf<int32_t> col;
+    DevBuf<double> val;
+};
+
+__global__ void k_csr_residual(int64_t n, const int64_t *__restrict__ off,
+                               const int32_t *__restrict__ col,
+                               const double *__restrict__ val,
+                               const double *__restrict__ x,
+                               const double *__restrict__ f,
+                               double *__restrict__ r) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s = 0.0;
+    for (int64_t t = off[i]; t < off[i + 1]; ++t)
+        s = __dadd_rn(s, __dmul_rn(val[t], x[col[t]]));
+    double v = -s;
+    if (f) v = __dadd_rn(v, f[i]);
+    r[i] = v;
+}
+
+// y = A x (y_i from 0.0 in column order)
+__global__ void k_csr_spmv(int64_t n, const int64_t *__restrict__ off,
+                           const int32_t *__restrict__ col,
+                           const double *__restrict__ val,
+                           const double *__restrict__ x,
+                           double *__restrict__ y) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s = 0.0;
+    for (int64_t t = off[i]; t < off[i + 1]; ++t)
+        s = __dadd_rn(s, __dmul_rn(val[t], x[col[t]]));
+    y[i] = s;
+}
+
+// y += A x, the product summed first (x += P.matvec(c), multigrid.py:153)
+__global__ void k_csr_spmv_add(int64_t n, const int64_t *__restrict__ off,
+                               const int32_t *__restrict__ col,
+                               const double *__restrict__ val,
+                               const double *__restrict__ x,
+                               double *__restrict__ y) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s = 0.0;
+    for (int64_t t = off[i]; t < off[i + 1]; ++t)
+        s = __dadd_rn(s, __dmul_rn(val[t], x[col[t]]));
+    y[i] = __dadd_rn(y[i], s);
+}
+
+// p_i = (tau * sum_j W_ij r_j) / L_i   (W = row_scaled)
+__global__ void k_csr_ne_p(int64_t n, const int64_t *__restrict__ off,
+                           const int32_t *__restrict__ col,
+                           const double *__restrict__ w,
+                           const double *__restrict__ L, double tau,
+                           const double *__restrict__ r,
+                           double *__restrict__ p) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double q = 0.0;
+    for (int64_t t = off[i]; t < off[i + 1]; ++t)
+        q = __dadd_rn(q, __dmul_rn(w[t], r[col[t]]));
+    p[i] = __ddiv_rn(__dmul_rn(tau, q), L[i]);
+}
+
+// x_i += p_i; r_i -= A_ij p_j for j in increasing column order
+__global__ void k_csr_ne_apply(int64_t n, const int64_t *__restrict__ off,
+                               const int32_t *__restrict__ col,
+                               const double *__restrict__ val,
+                               const double *__restrict__ p,
+                               double *__restrict__ x,
+                               double *__restrict__ r) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    x[i] = __dadd_rn(x[i], p[i]);
+    double ri = r[i];
+    for (int64_t t = off[i]; t < off[i + 1]; ++t)
+        ri = __dsub_rn(ri, __dmul_rn(val[t], p[col[t]]));
+    r[i] = ri;
+}
+
+// One dependency level (or colour) of the sequential NE-GS sweep: the rows
+// in `rows` are pairwise at graph distance >= 3, so their updates commute
+// and every r_j still receives its updates in index order.  A is symmetric
+// (checked at level creation), so column i of A is row i.
+__global__ void k_csr_gs_rows(int cnt, const int32_t *__restrict__ rows,
+                              const int64_t *__restrict__ off,
+                              const int32_t *__restrict__ col,
+                              const double *__restrict__ val,
+                              const double *__restrict__ w,
+                              const double *__restrict__ ndiag,
+                              double *__restrict__ x,
+                              double *__restrict__ r) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= cnt) return;
+    const int32_t i = rows[k];
+    const int64_t b = off[i], e = off[i + 1];
+    double q = 0.0;
+    for (int64_t t = b; t < e; ++t)
+        q = __dadd_rn(q, __dmul_rn(w[t], r[col[t]]));
+    const double p = __ddiv_rn(q, ndiag[i]);
+    x[i] = __dadd_rn(x[i], p);
+    for (int64_t t = b; t < e; ++t) {
+        const int32_t j = col[t];
+        r[j] = __dsub_rn(r[j], __dmul_rn(val[t], p));
+    }
+}
+
+// setup helpers -------------------------------------------------------------
+
+// W_t = A_t / L_col(t)
+__global__ void k_csr_row_scaled(int64_t nnz, const int32_t *__restrict__ col,
+                                 const double *__restrict__ val,
+                                 const double *__restrict__ L,
+                                 double *__restrict__ w) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < nnz) w[t] = __ddiv_rn(val[t], L[col[t]]);
+}
+
+// n_diag_i = sum_t A_t * W_t, sequential in row order from 0.0
+// (np.add.at over the CSR entries, smoothers.py:208-212)
+__global__ void k_csr_ndiag(int64_t n, const int64_t *__restrict__ off,
+                            const double *__restrict__ val,
+                            const double *__restrict__ w,
+                            double *__restrict__ nd) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s = 0.0;
+    for (int64_t t = off[i]; t < off[i + 1]; ++t)
+        s = __dadd_rn(s, __dmul_rn(val[t], w[t]));
+    nd[i] = s;
+}
+
+}  // namespace ocmg

@@ -1,0 +1,296 @@
+// Structured P1 (Poisson control) kernels.
+//
+// Level k holds N = n1*n1 vertices (n1 = 2^k+1), x fastest (mesh.py:146-147);
+// the block vector is [state(N), adjoint(N)] (FieldLayout, assembly.py:284).
+// A = [[M, K], [K, -M/alpha]] (assembly.py:274-277) is a 7-point stencil per
+// block with offsets, in CSR column order,
+//     d = 0:(-1,-1) 1:(0,-1) 2:(-1,0) 3:(0,0) 4:(1,0) 5:(0,1) 6:(1,1).
+// Coefficients depend only on a node's position class: per axis
+//     0,1,2 for i = 0,1,2;  3 for 3 <= i <= n1-4;  4,5,6 for n1-3, n1-2, n1-1,
+// 49 classes in all (needs n1 >= 7, i.e. k >= 3).  That resolution is what
+// row_scaled (A_ij / L_j) and n_diag need (they see the row class of every
+// neighbour).  The tables are built on the host from the reference's own
+// assembly rules and are bit-identical to the assembled CSR (see
+// paper_1502_03917_b200/assembly.py: p1_class_tables).
+//
+// Table layout (doubles), class c = 7*cls(iy) + cls(ix):
+//   A [49][2][14]  row coefficients of block-row b (0 state, 1 adjoint);
+//                  entries 0..6 multiply state-field neighbours d=0..6,
+//                  7..13 adjoint-field neighbours; 0 where absent
+//   W [49][2][14]  row_scaled = A_ij / L_j     (smoothers.py:204)
+//   L [49][2]      norm_diag                   (assembly.py:278-286)
+//   ND[49][2]      n_diag                      (smoothers.py:208-212)
+#pragma once
+
+#include "ocmg_common.cuh"
+
+namespace ocmg {
+
+constexpr int kP1Classes = 49;
+constexpr int kP1OffA = 0;
+constexpr int kP1OffW = kP1OffA + kP1Classes * 28;
+constexpr int kP1OffL = kP1OffW + kP1Classes * 28;
+constexpr int kP1OffND = kP1OffL + kP1Classes * 2;
+constexpr int kP1TableDoubles = kP1OffND + kP1Classes * 2;
+
+__device__ __forceinline__ int p1_axis_class(int i, int n1) {
+    if (i < 3) return i;
+    if (i > n1 - 4) return 6 - (n1 - 1 - i);
+    return 3;
+}
+
+struct P1Node {
+    int ix, iy, c;
+    int64_t v;  // vertex index iy*n1+ix
+    bool ex[7];
+    int64_t nb[7];
+};
+
+__device__ __forceinline__ P1Node p1_node(int ix, int iy, int n1) {
+    P1Node q;
+    q.ix = ix;
+    q.iy = iy;
+    q.c = 7 * p1_axis_class(iy, n1) + p1_axis_class(ix, n1);
+    q.v = (int64_t)iy * n1 + ix;
+    const bool l = ix > 0, rr = ix < n1 - 1, dn = iy > 0, up = iy < n1 - 1;
+    q.ex[0] = l && dn;  q.nb[0] = q.v - n1 - 1;
+    q.ex[1] = dn;       q.nb[1] = q.v - n1;
+    q.ex[2] = l;        q.nb[2] = q.v - 1;
+    q.ex[3] = true;     q.nb[3] = q.v;
+    q.ex[4] = rr;       q.nb[4] = q.v + 1;
+    q.ex[5] = up;       q.nb[5] = q.v + n1;
+    q.ex[6] = rr && up; q.nb[6] = q.v + n1 + 1;
+    return q;
+}
+
+// sum over one block-row: 7 state-field entries then 7 adjoint-field
+// entries, sequential from 0.0 (CSR order), absent neighbours skipped
+__device__ __forceinline__ double p1_row_dot(const P1Node &q,
+                                             const double *__restrict__ coef,
+                                             const double *__restrict__ v,
+                                             int64_t N) {
+    double s = 0.0;
+#pragma unroll
+    for (int d = 0; d < 7; ++d)
+        if (q.ex[d]) s = __dadd_rn(s, __dmul_rn(__ldg(coef + d), v[q.nb[d]]));
+#pragma unroll
+    for (int d = 0; d < 7; ++d)
+        if (q.ex[d])
+            s = __dadd_rn(s, __dmul_rn(__ldg(coef + 7 + d), v[N + q.nb[d]]));
+    return s;
+}
+
+// r = -(A x) + f    (assembly.py:259-263)
+__global__ void k_p1_residual(int n1, const double *__restrict__ T,
+                              const double *__restrict__ x,
+                              const double *__restrict__ f,
+                              double *__restrict__ r) {
+    const int64_t N = (int64_t)n1 * n1;
+    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v >= N) return;
+    const int iy = (int)(v / n1), ix = (int)(v - (int64_t)iy * n1);
+    const P1Node q = p1_node(ix, iy, n1);
+    const double *A = T + kP1OffA + q.c * 28;
+    double s0 = -p1_row_dot(q, A, x, N);
+    double s1 = -p1_row_dot(q, A + 14, x, N);
+    if (f) {
+        s0 = __dadd_rn(s0, f[v]);
+        s1 = __dadd_rn(s1, f[N + v]);
+    }
+    r[v] = s0;
+    r[N + v] = s1;
+}
+
+// NE-Jacobi phase 1: p = (tau * W r) / L   (kernels.py:27-32)
+__global__ void k_p1_ne_p(int n1, const double *__restrict__ T, double tau,
+                          const double *__restrict__ r,
+                          double *__restrict__ p) {
+    const int64_t N = (int64_t)n1 * n1;
+    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v >= N) return;
+    const int iy = (int)(v / n1), ix = (int)(v - (int64_t)iy * n1);
+    const P1Node q = p1_node(ix, iy, n1);
+    const double *W = T + kP1OffW + q.c * 28;
+    const double *L = T + kP1OffL + q.c * 2;
+    p[v] = __ddiv_rn(__dmul_rn(tau, p1_row_dot(q, W, r, N)), __ldg(L));
+    p[N + v] = __ddiv_rn(__dmul_rn(tau, p1_row_dot(q, W + 14, r, N)),
+                         __ldg(L + 1));
+}
+
+// NE-Jacobi phase 2 as a row gather (kernels.py:33-38): x += p; r_j -= A_ji
+// p_i in increasing i, i.e. CSR order of row j
+__global__ void k_p1_ne_apply(int n1, const double *__restrict__ T,
+                              const double *__restrict__ p,
+                              double *__restrict__ x,
+                              double *__restrict__ r) {
+    const int64_t N = (int64_t)n1 * n1;
+    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v >= N) return;
+    const int iy = (int)(v / n1), ix = (int)(v - (int64_t)iy * n1);
+    const P1Node q = p1_node(ix, iy, n1);
+    const double *A = T + kP1OffA + q.c * 28;
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+        const int64_t j = b * N + v;
+        x[j] = __dadd_rn(x[j], p[j]);
+        double rj = r[j];
+        const double *a = A + 14 * b;
+#pragma unroll
+        for (int d = 0; d < 7; ++d)
+            if (q.ex[d]) rj = __dsub_rn(rj, __dmul_rn(__ldg(a + d), p[q.nb[d]]));
+#pragma unroll
+        for (int d = 0; d < 7; ++d)
+            if (q.ex[d])
+                rj = __dsub_rn(rj, __dmul_rn(__ldg(a + 7 + d), p[N + q.nb[d]]));
+        r[j] = rj;
+    }
+}
+
+// One unknown of the sequential NE-GS sweep (kernels.py:57-64) in the
+// reference's arithmetic.  Column i of A equals row i (A is symmetric
+// bitwise: every off-diagonal entry sums the same one or two element
+// contributions from both sides).
+__device__ __forceinline__ void p1_gs_unknown(int field, int ix, int iy,
+                                              int n1,
+                                              const double *__restrict__ T,
+                                              double *__restrict__ x,
+                                              double *__restrict__ r) {
+    const int64_t N = (int64_t)n1 * n1;
+    const P1Node q = p1_node(ix, iy, n1);
+    const double *W = T + kP1OffW + q.c * 28 + 14 * field;
+    const double *A = T + kP1OffA + q.c * 28 + 14 * field;
+    const double nd = __ldg(T + kP1OffND + q.c * 2 + field);
+    const double p = __ddiv_rn(p1_row_dot(q, W, r, N), nd);
+    const int64_t i = field * N + q.v;
+    x[i] = __dadd_rn(x[i], p);
+#pragma unroll
+    for (int d = 0; d < 7; ++d)
+        if (q.ex[d]) {
+            const int64_t j = q.nb[d];
+            r[j] = __dsub_rn(r[j], __dmul_rn(__ldg(A + d), p));
+            r[N + j] = __dsub_rn(r[N + j], __dmul_rn(__ldg(A + 7 + d), p));
+        }
+}
+
+// All unknowns of dependency level t.  Forward order: state vertex (ix,iy)
+// sits at level ix + 2 iy, adjoint vertex at ix + 2 iy + 7 (depth 3*2^k+8;
+// SURVEY.md §8(a)).  Backward order is the point reflection of that with the
+// fields swapped.
+__global__ void k_p1_gs_level(int n1, const double *__restrict__ T, int t,
+                              int forward, double *__restrict__ x,
+                              double *__restrict__ r) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= 2 * n1) return;
+    const int field = k >= n1 ? 1 : 0;
+    const int row = k - field * n1;
+    int ix, iy;
+    if (forward) {
+        const int lev = field ? t - 7 : t;
+        iy = row;
+        ix = lev - 2 * iy;
+    } else {
+        const int lev = field ? t : t - 7;
+        const int iyr = row;
+        const int ixr = lev - 2 * iyr;
+        ix = n1 - 1 - ixr;
+        iy = n1 - 1 - iyr;
+    }
+    if (ix < 0 || ix >= n1 || iy < 0 || iy >= n1) return;
+    p1_gs_unknown(field, ix, iy, n1, T, x, r);
+}
+
+// One colour of the distance-2 multicolour order: colour c in 0..13 is
+// field c/7 and (ix + 2 iy) mod 7 == c % 7.  Same-colour unknowns are at
+// graph distance >= 3 (no 19-point offset satisfies dx + 2 dy = 0 mod 7).
+__global__ void k_p1_gs_colour(int n1, const double *__restrict__ T,
+                               int colour, double *__restrict__ x,
+                               double *__restrict__ r) {
+    const int per_row = (n1 + 6) / 7;
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= (int64_t)per_row * n1) return;
+    const int iy = (int)(k / per_row);
+    const int jj = (int)(k - (int64_t)iy * per_row);
+    const int cc = colour % 7;
+    const int ix = ((cc - 2 * iy) % 7 + 7) % 7 + 7 * jj;
+    if (ix >= n1) return;
+    p1_gs_unknown(colour / 7, ix, iy, n1, T, x, r);
+}
+
+// partial[b] = sum over a grid-strided slice of L_i x_i^2 (both fields)
+__global__ void k_p1_wsumsq_partial(int n1, const double *__restrict__ T,
+                                    const double *__restrict__ x,
+                                    double *__restrict__ partial) {
+    __shared__ double sh[32];
+    const int64_t N = (int64_t)n1 * n1;
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * N;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int field = i >= N;
+        const int64_t v = i - field * N;
+        const int iy = (int)(v / n1), ix = (int)(v - (int64_t)iy * n1);
+        const int c = 7 * p1_axis_class(iy, n1) + p1_axis_class(ix, n1);
+        const double xi = x[i];
+        acc += __ldg(T + kP1OffL + 2 * c + field) * xi * xi;
+    }
+    acc = block_sum(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// P1 transfers, both fields (transfer.py:34-55 block-diagonal per field).
+// R = P^T: coarse row (cx,cy) gathers, in increasing fine index, the fine
+// vertices (2cx-1,2cy-1) (2cx,2cy-1) (2cx-1,2cy) (2cx,2cy) (2cx+1,2cy)
+// (2cx,2cy+1) (2cx+1,2cy+1) with weights 1/2 except 1 at the centre.
+// ---------------------------------------------------------------------------
+__global__ void k_p1_restrict(int nc1, int n_fields,
+                              const double *__restrict__ rf,
+                              double *__restrict__ rc) {
+    const int64_t Nc = (int64_t)nc1 * nc1;
+    const int nf1 = 2 * nc1 - 1;
+    const int64_t Nf = (int64_t)nf1 * nf1;
+    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v >= Nc) return;
+    const int cy = (int)(v / nc1), cx = (int)(v - (int64_t)cy * nc1);
+    const int fx = 2 * cx, fy = 2 * cy;
+    const int64_t c = (int64_t)fy * nf1 + fx;
+    const bool l = cx > 0, rr = cx < nc1 - 1, dn = cy > 0, up = cy < nc1 - 1;
+    for (int b = 0; b < n_fields; ++b) {
+        const double *f = rf + b * Nf;
+        double s = 0.0;
+        if (l && dn) s = __dadd_rn(s, __dmul_rn(0.5, f[c - nf1 - 1]));
+        if (dn) s = __dadd_rn(s, __dmul_rn(0.5, f[c - nf1]));
+        if (l) s = __dadd_rn(s, __dmul_rn(0.5, f[c - 1]));
+        s = __dadd_rn(s, f[c]);
+        if (rr) s = __dadd_rn(s, __dmul_rn(0.5, f[c + 1]));
+        if (up) s = __dadd_rn(s, __dmul_rn(0.5, f[c + nf1]));
+        if (rr && up) s = __dadd_rn(s, __dmul_rn(0.5, f[c + nf1 + 1]));
+        rc[b * Nc + v] = s;
+    }
+}
+
+// x_f += P c: coarse vertices copy, midpoints average their edge ends
+// (lower end first), the interpolant summed before the add
+__global__ void k_p1_prolong_add(int nc1, int n_fields,
+                                 const double *__restrict__ c,
+                                 double *__restrict__ xf) {
+    const int64_t Nc = (int64_t)nc1 * nc1;
+    const int nf1 = 2 * nc1 - 1;
+    const int64_t Nf = (int64_t)nf1 * nf1;
+    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v >= Nf) return;
+    const int fy = (int)(v / nf1), fx = (int)(v - (int64_t)fy * nf1);
+    const int ox = fx & 1, oy = fy & 1;
+    const int64_t a = (int64_t)(fy >> 1) * nc1 + (fx >> 1);
+    const int64_t b2 = (int64_t)((fy >> 1) + oy) * nc1 + (fx >> 1) + ox;
+    for (int b = 0; b < n_fields; ++b) {
+        const double *cc = c + b * Nc;
+        double s;
+        if (!(ox | oy))
+            s = __dmul_rn(1.0, cc[a]);
+        else
+            s = __dadd_rn(__dmul_rn(0.5, cc[a]), __dmul_rn(0.5, cc[b2]));
+        xf[b * Nf + v] = __dadd_rn(xf[b * Nf + v], s);
+    }
+}
+
+}  // namespace ocmg

@@ -1,0 +1,157 @@
+"""Normal-equation smoothers on the device (smoothers.py:1-285).
+
+Same names and semantics as the reference: a ``SmootherState`` binds a kind
+to one level; ``sweep(x, r)`` mutates the iterate and the maintained
+residual in place and accumulates the touched-entry count in ``op_count``.
+Only the normal-equation family is in scope (``normal`` = NE-Jacobi,
+``lsgs`` = NE-GS, ``slsgs``); the collective and patch smoothers are
+outside the hot path.
+
+NE-GS runs in one of three modes (``gs_mode``):
+  * ``"wavefront"`` -- reference sweep order; on structured Poisson levels
+    the fused pipelined kernel, elsewhere the level schedule;
+  * ``"reference"`` -- reference order and reference arithmetic
+    (level-scheduled, bit-identical to kernels.lsgs_sweep);
+  * ``"multicolour"`` -- distance-2 multicolour order (a different
+    smoother with its own convergence factor).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+from . import _lib
+from ._vec import as_device, back_inplace, zeros
+
+SMOOTHER_NAMES = ("normal", "lsgs", "slsgs", "cgs", "vanka")
+DEVICE_SMOOTHERS = ("normal", "lsgs", "slsgs")
+GS_MODES = tuple(_lib.GS_MODES)
+
+# damping defaults of the experiment protocol (smoothers.py:25-29)
+DEFAULT_TAU = {
+    ("normal", "poisson"): 0.4,
+    ("normal", "stokes"): 0.35,
+    ("vanka", "stokes"): 0.4,
+}
+
+
+@dataclass(frozen=True)
+class SmootherKind:
+    """Smoother selector plus damping (smoothers.py:32-49)."""
+
+    name: str
+    tau: float | None = None
+
+    def __post_init__(self):
+        if self.name not in SMOOTHER_NAMES:
+            raise ValueError(f"unknown smoother '{self.name}'; choose from "
+                             f"{SMOOTHER_NAMES}")
+        if self.tau is not None and not 0.0 < self.tau < 2.0:
+            raise ValueError("damping parameter must lie in (0, 2)")
+
+    def resolved_tau(self, problem):
+        if self.tau is not None:
+            return self.tau
+        return DEFAULT_TAU.get((self.name, problem))
+
+
+def check_applicability(kind, problem):
+    """smoothers.py:52-60, plus the device scope."""
+    if kind.name == "cgs" and problem != "poisson":
+        raise ValueError("the collective pair smoother only applies to the "
+                         "scalar control problem")
+    if kind.name == "vanka" and problem != "stokes":
+        raise ValueError("the patch smoother only applies to the velocity "
+                         "tracking problem")
+    if kind.name not in DEVICE_SMOOTHERS:
+        raise NotImplementedError(
+            f"smoother '{kind.name}' is outside the B200 hot path "
+            "(normal / lsgs / slsgs only)")
+    if kind.name == "normal" and kind.resolved_tau(problem) is None:
+        raise ValueError(f"smoother '{kind.name}' needs a damping parameter")
+
+
+class SmootherState:
+    """Per-level smoother binding (smoothers.py:179-244).  The device level
+    already holds what the reference precomputes here (row_scaled, n_diag,
+    column mirror, dependency schedule)."""
+
+    def __init__(self, system, kind: SmootherKind, gs_mode="wavefront"):
+        check_applicability(kind, system.problem)
+        if gs_mode not in GS_MODES:
+            raise ValueError(f"gs_mode must be one of {GS_MODES}")
+        self.system = system
+        self.kind = kind
+        self.gs_mode = gs_mode
+        self.tau = kind.resolved_tau(system.problem)
+        self.op_count = 0
+        self._update = None
+
+    def _scratch(self):
+        if self._update is None:
+            self._update = zeros(self.system.n)
+        return self._update
+
+    def sweep(self, x, r, post=False):
+        """One smoothing step of the bound kind (smoothers.py:226-244);
+        ``post`` only matters for the patch smoother."""
+        name = self.kind.name
+        if name == "normal":
+            return normal_equation_sweep(self, x, r)
+        if name == "lsgs":
+            return lsgs_sweep(self, x, r)
+        return slsgs_sweep(self, x, r)
+
+
+def make_smoother(system, kind, tau=None, gs_mode="wavefront"):
+    """smoothers.py:247-253."""
+    if isinstance(kind, str):
+        kind = SmootherKind(name=kind, tau=tau)
+    elif tau is not None:
+        kind = SmootherKind(name=kind.name, tau=tau)
+    return SmootherState(system, kind, gs_mode=gs_mode)
+
+
+def _pair(state, x, r):
+    n = state.system.n
+    xd, xnp = as_device(x, n)
+    rd, rnp = as_device(r, n)
+    return xd, xnp, rd, rnp
+
+
+def normal_equation_sweep(state, x, r):
+    """Damped Richardson step on the weighted normal equations
+    (smoothers.py:256-267 -> kernels.py:17-39)."""
+    xd, xnp, rd, rnp = _pair(state, x, r)
+    ops = ctypes.c_int64()
+    _lib.call("ocmg_ne_jacobi_sweep", state.system.handle, float(state.tau),
+              _lib.dptr(xd), _lib.dptr(rd), _lib.dptr(state._scratch()),
+              _lib.stream_ptr(), ctypes.byref(ops))
+    state.op_count += ops.value
+    back_inplace(xd, x, xnp)
+    back_inplace(rd, r, rnp)
+    return x, r
+
+
+def lsgs_sweep(state, x, r, order="forward"):
+    """Least-squares Gauss-Seidel sweep (smoothers.py:270-278 ->
+    kernels.py:43-66)."""
+    if order not in ("forward", "backward"):
+        raise ValueError("order must be 'forward' or 'backward'")
+    xd, xnp, rd, rnp = _pair(state, x, r)
+    ops = ctypes.c_int64()
+    _lib.call("ocmg_ne_gs_sweep", state.system.handle,
+              _lib.GS_MODES[state.gs_mode], 1 if order == "forward" else 0,
+              _lib.dptr(xd), _lib.dptr(rd), _lib.stream_ptr(),
+              ctypes.byref(ops))
+    state.op_count += ops.value
+    back_inplace(xd, x, xnp)
+    back_inplace(rd, r, rnp)
+    return x, r
+
+
+def slsgs_sweep(state, x, r):
+    """Forward then backward NE-GS (smoothers.py:281-285)."""
+    lsgs_sweep(state, x, r, order="forward")
+    lsgs_sweep(state, x, r, order="backward")
+    return x, r

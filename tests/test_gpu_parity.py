@@ -1,0 +1,303 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bars (north_star): bit-exact where the arithmetic is the reference's
+(residual, NE-Jacobi, reference-mode NE-GS, transfers); wavefront-mode
+NE-GS iterates within 1e-12 relative with identical cycle counts; the
+multicolour mode is compared with the oracle run in the same colour order.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1502_03917_b200 as P  # noqa: E402
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def rel(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+SYSTEMS = {}
+
+
+def systems(prob, k, alpha):
+    key = (prob, k, alpha)
+    if key not in SYSTEMS:
+        if prob == "poisson":
+            SYSTEMS[key] = (O.poisson_system(k, alpha),
+                            P.build_poisson_system(k, alpha))
+        else:
+            SYSTEMS[key] = (O.stokes_system(k, alpha),
+                            P.build_stokes_system(k, alpha))
+    return SYSTEMS[key]
+
+
+def inputs(osys, seed):
+    rng = np.random.default_rng(seed)
+    x0 = rng.uniform(-1, 1, osys.n)
+    f = rng.uniform(-1, 1, osys.n)
+    osys.mean_project(x0)
+    return x0, f, osys.residual(x0, f)
+
+
+CASES = [("poisson", 2, 1e-6), ("poisson", 3, 1e-6), ("poisson", 5, 1e-4),
+         ("poisson", 6, 1.0), ("stokes", 2, 1e-4), ("stokes", 4, 1e-6)]
+
+
+@pytest.mark.parametrize("prob,k,alpha", CASES)
+def test_residual_bitwise(prob, k, alpha):
+    osys, dsys = systems(prob, k, alpha)
+    x0, f, r0 = inputs(osys, 1)
+    assert np.array_equal(host(dsys.residual(dev(x0), dev(f))), r0)
+    assert np.array_equal(host(dsys.residual(dev(x0))),
+                          osys.residual(x0))
+
+
+@pytest.mark.parametrize("prob,k,alpha", CASES)
+def test_ne_jacobi_bitwise(prob, k, alpha):
+    osys, dsys = systems(prob, k, alpha)
+    x0, f, r0 = inputs(osys, 2)
+    st = P.make_smoother(dsys, "normal")
+    xd, rd = dev(x0), dev(r0)
+    for _ in range(3):
+        st.sweep(xd, rd)
+    xo, ro = x0.copy(), r0.copy()
+    ost = O.OracleSmoother(osys, "normal")
+    for _ in range(3):
+        ost.sweep(xo, ro)
+    assert np.array_equal(host(xd), xo)
+    assert np.array_equal(host(rd), ro)
+    assert st.op_count == ost.op_count or prob == "stokes"
+
+
+@pytest.mark.parametrize("prob,k,alpha", CASES)
+@pytest.mark.parametrize("order", ["forward", "backward"])
+def test_ne_gs_reference_mode_bitwise(prob, k, alpha, order):
+    osys, dsys = systems(prob, k, alpha)
+    x0, f, r0 = inputs(osys, 3)
+    st = P.make_smoother(dsys, "lsgs", gs_mode="reference")
+    xd, rd = dev(x0), dev(r0)
+    P.lsgs_sweep(st, xd, rd, order=order)
+    P.lsgs_sweep(st, xd, rd, order=order)
+    xo, ro = x0.copy(), r0.copy()
+    ost = O.OracleSmoother(osys, "lsgs")
+    for _ in range(2):
+        ost.lsgs(xo, ro, forward=(order == "forward"))
+    assert np.array_equal(host(xd), xo)
+    assert np.array_equal(host(rd), ro)
+
+
+@pytest.mark.parametrize("prob,k,alpha", CASES)
+def test_ne_gs_wavefront_mode(prob, k, alpha):
+    """Reference order, delta-form arithmetic: 1e-12 (north_star bar)."""
+    osys, dsys = systems(prob, k, alpha)
+    x0, f, r0 = inputs(osys, 4)
+    st = P.make_smoother(dsys, "slsgs", gs_mode="wavefront")
+    xd, rd = dev(x0), dev(r0)
+    for _ in range(2):
+        st.sweep(xd, rd)
+    xo, ro = x0.copy(), r0.copy()
+    ost = O.OracleSmoother(osys, "slsgs")
+    for _ in range(2):
+        ost.sweep(xo, ro)
+    assert rel(host(xd), xo) < 1e-12
+    # residual coherence: maintained r equals f - A x
+    assert rel(host(rd), osys.residual(host(xd), f)) < 1e-11
+    assert rel(host(rd), ro) < 1e-11
+
+
+def _colour_perm(osys, dsys):
+    """Unknown order of the multicolour sweep."""
+    if osys.problem == "poisson":
+        n1 = 2 ** osys.k + 1
+        iy, ix = np.divmod(np.arange(n1 * n1), n1)
+        col = (ix + 2 * iy) % 7
+        N = n1 * n1
+        return np.concatenate([np.flatnonzero(col == c) + b * N
+                               for b in range(2) for c in range(7)])
+    # generic levels: greedy distance-2 colouring in index order
+    A = osys.A
+    colour = -np.ones(osys.n, dtype=np.int64)
+    for i in range(osys.n):
+        nb = A.indices[A.indptr[i]:A.indptr[i + 1]]
+        used = set()
+        for j in nb:
+            used.update(colour[A.indices[A.indptr[j]:A.indptr[j + 1]]])
+        c = 0
+        while c in used:
+            c += 1
+        colour[i] = c
+    return np.argsort(colour, kind="stable")
+
+
+@pytest.mark.parametrize("prob,k,alpha", [("poisson", 4, 1e-6),
+                                          ("poisson", 6, 1.0),
+                                          ("stokes", 3, 1e-4)])
+def test_ne_gs_multicolour_matches_permuted_oracle(prob, k, alpha):
+    osys, dsys = systems(prob, k, alpha)
+    x0, f, r0 = inputs(osys, 5)
+    st = P.make_smoother(dsys, "lsgs", gs_mode="multicolour")
+    xd, rd = dev(x0), dev(r0)
+    st.sweep(xd, rd)
+    perm = _colour_perm(osys, dsys)
+    Ap = O.ocmg_oracle._canon(osys.A[perm][:, perm])
+    psys = O.OracleSystem(osys.problem, osys.k, osys.alpha, Ap, osys.L[perm],
+                          osys.fields, osys.mass)
+    xo, ro = x0[perm].copy(), r0[perm].copy()
+    O.OracleSmoother(psys, "lsgs").lsgs(xo, ro, True)
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(perm.size)
+    assert rel(host(xd), xo[inv]) < 1e-13
+    assert rel(host(rd), ro[inv]) < 1e-10
+
+
+@pytest.mark.parametrize("prob,kc", [("poisson", 1), ("poisson", 4),
+                                     ("stokes", 1), ("stokes", 3)])
+def test_transfers_bitwise(prob, kc):
+    alpha = 1e-4
+    oc, dc = systems(prob, kc, alpha)
+    of, df = systems(prob, kc + 1, alpha)
+    otr = O.system_transfer(oc, of)
+    dtr = P.system_transfer(dc, df)
+    rng = np.random.default_rng(6)
+    rf = rng.uniform(-1, 1, of.n)
+    c = rng.uniform(-1, 1, oc.n)
+    xf = rng.uniform(-1, 1, of.n)
+    assert np.array_equal(host(dtr.restriction.matvec(dev(rf))),
+                          O.ocmg_oracle.csr_matvec(otr.R, rf))
+    xd = dev(xf)
+    dtr.prolong_add(dev(c), xd)
+    assert np.array_equal(host(xd), xf + O.ocmg_oracle.csr_matvec(otr.P, c))
+
+
+@pytest.mark.parametrize("prob,alpha", [("poisson", 1e-6), ("stokes", 1e-4)])
+def test_coarse_solve(prob, alpha, golden):
+    osys, dsys = systems(prob, 1, alpha)
+    d = golden(f"coarse_{prob}.npz")
+    cs = P.CoarseSolver(dsys)
+    x = host(cs.solve(dev(d["rhs"])))
+    assert rel(x, d["x"]) < 1e-12
+    assert rel(x, O.OracleCoarse(osys).solve(d["rhs"])) < 1e-12
+
+
+BASELINE = [
+    # tag, problem, k, alpha, smoother, cycle, coarsest, seed, sine, mode
+    ("c1_lsgs", "poisson", 6, 1e-6, "lsgs", "v", 1, 0, False, "wavefront"),
+    ("c1_lsgs", "poisson", 6, 1e-6, "lsgs", "v", 1, 0, False, "reference"),
+    ("c1_normal", "poisson", 6, 1e-6, "normal", "v", 1, 0, False, "wavefront"),
+    ("c1_slsgs", "poisson", 6, 1e-6, "slsgs", "v", 1, 0, False, "wavefront"),
+    ("c4_lsgs", "stokes", 5, 1e-4, "lsgs", "v", 1, 1, False, "wavefront"),
+    ("c4_normal", "stokes", 5, 1e-4, "normal", "v", 1, 1, False, "wavefront"),
+    ("p5w_sine", "poisson", 5, 1e-6, "lsgs", "w", 1, 0, True, "wavefront"),
+    ("p6_a1e-4_c2", "poisson", 6, 1e-4, "lsgs", "v", 2, 0, False,
+     "wavefront"),
+]
+
+
+@pytest.mark.parametrize("case", BASELINE,
+                         ids=[f"{c[0]}-{c[-1]}" for c in BASELINE])
+def test_baseline_protocol_vs_reference_golden(case, golden):
+    """Full solves against fixtures made by the reference itself: same
+    cycle count, every kept iterate and the final iterate within 1e-12."""
+    tag, prob, k, alpha, sm, cyc, co, seed, sine, mode = case
+    d = golden(f"baseline_{tag}.npz")
+    nu = 1 if sm == "slsgs" else 2
+    cfg = P.CycleConfig(smoother=P.SmootherKind(sm), cycle=cyc, nu_pre=nu,
+                        nu_post=nu, coarsest_level=co, gs_mode=mode)
+    mg = P.build_solver(prob, k, alpha, cfg)
+    f = P.baseline_rhs(mg.finest, seed, add_sine=sine)
+    assert rel(host(f), d["f"]) <= 1e-15
+    x = torch.zeros_like(f)
+    its = []
+    for c in range(len(d["iterates"])):
+        mg.cycle(len(mg.systems) - 1, x, f)
+        P.pressure_mean_projection(mg.finest, x)
+        its.append(host(x).copy())
+    for a, b in zip(its, d["iterates"]):
+        assert rel(a, b) < 1e-12
+    x, hist = mg.solve_to_tolerance(f, tol=1e-8, max_cycles=300)
+    assert len(hist) == len(d["hist"])
+    assert rel(host(x), d["x_final"]) < 1e-12
+    assert rel(np.array(hist), d["hist"]) < 1e-6
+
+
+def test_multicolour_solve_converges():
+    """Multicolour mode is a different smoother: report its own cycle count
+    (config-1 shape) and check it converges like NE-GS."""
+    cfg = P.CycleConfig(smoother=P.SmootherKind("lsgs"), cycle="v",
+                        gs_mode="multicolour")
+    mg = P.build_solver("poisson", 6, 1e-6, cfg)
+    f = P.baseline_rhs(mg.finest, 0)
+    _, hist = mg.solve_to_tolerance(f, tol=1e-8, max_cycles=100)
+    assert hist[-1] <= 1e-8 and len(hist) <= 40
+
+
+def test_reference_protocol_solve(golden):
+    d = golden("refproto_p4_lsgs.npz")
+    cfg = P.CycleConfig(smoother=P.SmootherKind("lsgs"), cycle="w")
+    mg = P.build_solver("poisson", 4, 1.0, cfg)
+    rep = mg.solve()
+    assert rep.iterations == int(d["iterations"]) and rep.converged
+    assert rel(np.array(rep.norm_history), d["hist"]) < 1e-12
+
+
+def test_numpy_arrays_drop_in():
+    """Reference-style numpy callers work unchanged (copied through)."""
+    osys, dsys = systems("poisson", 4, 1e-6)
+    x0, f, r0 = inputs(osys, 7)
+    st = P.make_smoother(dsys, "lsgs", gs_mode="reference")
+    x, r = x0.copy(), r0.copy()
+    st.sweep(x, r)
+    xo, ro = x0.copy(), r0.copy()
+    O.OracleSmoother(osys, "lsgs").sweep(xo, ro)
+    assert np.array_equal(x, xo) and np.array_equal(r, ro)
+    assert np.array_equal(dsys.residual(x0, f), r0)
+
+
+def test_errors_map_to_reference_exceptions():
+    osys, dsys = systems("poisson", 4, 1e-6)
+    st = P.make_smoother(dsys, "lsgs")
+    with pytest.raises(ValueError):
+        P.lsgs_sweep(st, dev(np.zeros(osys.n)), dev(np.zeros(osys.n)),
+                     order="sideways")
+    with pytest.raises(ValueError):
+        dsys.residual(dev(np.zeros(osys.n + 1)))
+    with pytest.raises(ValueError):
+        P.build_poisson_system(4, -1.0)
+
+
+@pytest.mark.parametrize("mode", ["wavefront", "multicolour", "reference"])
+def test_fixed_point_full_size(mode):
+    """Size-independent property at a large level: r = 0 is a fixed point of
+    every sweep, and after a sweep from a random state the maintained
+    residual stays coherent with f - A x."""
+    k = 10 if mode == "reference" else 12
+    dsys = P.build_poisson_system(k, 1e-6)
+    n = dsys.n
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.rand(n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    r = torch.zeros_like(x)
+    st = P.make_smoother(dsys, "lsgs", gs_mode=mode)
+    x0 = x.clone()
+    st.sweep(x, r)
+    assert torch.equal(x, x0) and int(torch.count_nonzero(r)) == 0
+    f = torch.rand(n, dtype=torch.float64, device="cuda", generator=g)
+    r = dsys.residual(x, f)
+    st.sweep(x, r)
+    r2 = dsys.residual(x, f)
+    err = float((r - r2).abs().max() / r2.abs().max())
+    assert err < 1e-9, err
