@@ -382,8 +382,8 @@ class BlockSystem:
     def residual(self, x, rhs=None):
         """r = rhs - A x (assembly.py:259-263), on the device."""
         from ._vec import as_device, back
-        xd, was_np = as_device(x)
-        fd = as_device(rhs)[0] if rhs is not None else None
+        xd, was_np = as_device(x, self.n)
+        fd = as_device(rhs, self.n)[0] if rhs is not None else None
         import torch
         r = torch.empty_like(xd)
         _lib.call("ocmg_residual", self.handle, _lib.dptr(xd),
