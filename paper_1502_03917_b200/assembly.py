@@ -393,7 +393,7 @@ class BlockSystem:
     def norm(self, x):
         """sqrt(sum L_i x_i^2) (assembly.py:265-267)."""
         from ._vec import as_device, device_scalar
-        xd, _ = as_device(x)
+        xd, _ = as_device(x, self.n)
         out = device_scalar()
         _lib.call("ocmg_norm2", self.handle, _lib.dptr(xd), 1,
                   _lib.dptr(out), _lib.stream_ptr())
@@ -488,7 +488,7 @@ def pressure_mean_projection(system, x):
     if system.problem != "stokes":
         return x
     from ._vec import as_device, back_inplace
-    xd, was_np = as_device(x)
+    xd, was_np = as_device(x, system.n)
     _lib.call("ocmg_mean_project", system.handle, _lib.dptr(xd),
               _lib.stream_ptr())
     back_inplace(xd, x, was_np)

@@ -570,7 +570,7 @@ int ocmg_level_create_p1(int k, double alpha, const double *tables,
         lv->nnz = 4 * pairs;
         lv->field_off = {0, N, 2 * N};
         lv->tables.upload(tables, n_tables);
-        lv->wf.init(lv->k, lv->n1, lv->tables.p + kP1TableDoubles);
+        lv->wf.init(lv->k, lv->n1, lv->tables.p, lv->tables.p + kP1TableDoubles);
         lv->partial.alloc(kRedGrid);
         lv->scal.alloc(8);
         *out = lv.release();
@@ -835,3 +835,37 @@ int ocmg_solve(ocmg_hierarchy *h, double *x, const double *f, double tol,
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// internal debug hook (not part of the ABI in include/ocmg_b200.h): copies a
+// wavefront ring buffer (0: chain-1 p, 1: chain-2 p, 2: u) to `out` (device)
+// ---------------------------------------------------------------------------
+extern "C" int ocmg__debug_wf_ring(const ocmg_level *lv, int which, double *out,
+                                   int64_t *count) {
+    return guarded([&] {
+        OCMG_REQUIRE(lv && lv->kind == kP1 && lv->wf.ready(), "no wavefront");
+        const DevBuf<double> &src =
+            which == 0 ? lv->wf.ring1 : which == 1 ? lv->wf.ring2 : lv->wf.ringu;
+        *count = (int64_t)src.n;
+        if (out)
+            OCMG_CUDA(cudaMemcpy(out, src.p, src.n * sizeof(double),
+                                 cudaMemcpyDeviceToDevice));
+    });
+}
+
+// internal: per-warp iteration timestamps of the last wavefront sweep
+// (only when built with -DOCMG_WF_PROFILE); returns nb, niter, nwarps
+extern "C" int ocmg__debug_wf_prof(const ocmg_level *lv, unsigned long long *out,
+                                   int64_t *dims) {
+    return guarded([&] {
+        OCMG_REQUIRE(lv && lv->kind == kP1 && lv->wf.ready(), "no wavefront");
+        dims[0] = lv->wf.nb;
+        dims[1] = lv->wf.niter;
+        dims[2] = wf::NWARPS;
+        dims[3] = (int64_t)lv->wf.prof.n;
+        if (out && lv->wf.prof.n)
+            OCMG_CUDA(cudaMemcpy(out, lv->wf.prof.p,
+                                 lv->wf.prof.n * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost));
+    });
+}

@@ -120,6 +120,32 @@ def test_ne_gs_wavefront_mode(prob, k, alpha):
     assert rel(host(rd), ro) < 1e-11
 
 
+@pytest.mark.parametrize("k", [7, 8, 10, 12])
+@pytest.mark.parametrize("order", ["forward", "backward"])
+def test_wavefront_vs_reference_mode_many_bands(k, order):
+    """The fused wavefront kernel against the bitwise reference-order path at
+    levels with many bands (L12: 129 bands of 32 rows)."""
+    dsys = P.build_poisson_system(k, 1e-6)
+    g = torch.Generator(device="cuda").manual_seed(k)
+    x0 = torch.rand(dsys.n, dtype=torch.float64, device="cuda",
+                    generator=g) - 0.5
+    f = torch.rand(dsys.n, dtype=torch.float64, device="cuda", generator=g)
+    r0 = dsys.residual(x0, f)
+    out = {}
+    for mode in ("wavefront", "reference"):
+        st = P.make_smoother(dsys, "lsgs", gs_mode=mode)
+        x, r = x0.clone(), r0.clone()
+        for _ in range(2):
+            P.lsgs_sweep(st, x, r, order=order)
+        out[mode] = (x, r)
+    xw, rw = out["wavefront"]
+    xr, rr = out["reference"]
+    ex = float((xw - xr).abs().max() / xr.abs().max())
+    er = float((rw - rr).abs().max() / rr.abs().max())
+    assert ex < 1e-12, ex
+    assert er < 1e-10, er
+
+
 def _colour_perm(osys, dsys):
     """Unknown order of the multicolour sweep."""
     if osys.problem == "poisson":
