@@ -12,6 +12,8 @@
 #include "ocmg_common.cuh"
 #include "ocmg_csr.cuh"
 #include "ocmg_p1.cuh"
+#include "ocmg_p1_tiled.cuh"
+#include "ocmg_p1_mc.cuh"
 #include "ocmg_wavefront.cuh"
 
 using namespace ocmg;
@@ -58,7 +60,13 @@ struct ocmg_level {
     int k = 0, n1 = 0;
     double alpha = 0.0;
     DevBuf<double> tables;
+    P1Coef28 cA{}, cW{};  // class-(3,3) A and row_scaled rows (tiled kernels)
+    double cL[2] = {0.0, 0.0};
     P1Wavefront wf;
+    McsPlan mc;               // one-launch multicolour sweep geometry
+    DevBuf<double> mc_r;      // its out-of-place residual
+    DevBuf<double> mc_coef;   // [49][2][29] W row, A row, n_diag
+    double mc_ci[58] = {};    // its class-(3,3) rows
     // reduction scratch
     DevBuf<double> partial, scal;
 };
@@ -201,11 +209,18 @@ void csr_transpose(int64_t nrows, int64_t ncols, const int64_t *off,
 
 constexpr int kBlk = 256;
 
+dim3 p1_interior_grid(int n1) {
+    const int m = n1 - 2 * kRing;
+    return dim3((m + kTX - 1) / kTX, (m + kTY * kRPT - 1) / (kTY * kRPT));
+}
+
 void level_residual(const ocmg_level *lv, const double *x, const double *f,
                     double *r, cudaStream_t s) {
     if (lv->kind == kP1) {
-        OCMG_LAUNCH(k_p1_residual, grid_for((int64_t)lv->n1 * lv->n1, kBlk), kBlk, 0, s, 
-            lv->n1, lv->tables.p, x, f, r);
+        const dim3 g = p1_interior_grid(lv->n1), b(kTX, kTY);
+        OCMG_LAUNCH(k_p1_residual_int, g, b, 0, s, lv->n1, lv->cA, x, f, r);
+        OCMG_LAUNCH(k_p1_residual_ring, grid_for(p1_ring_count(lv->n1, kRing), kBlk),
+                    kBlk, 0, s, lv->n1, lv->tables.p, x, f, r);
     } else {
         OCMG_LAUNCH(k_csr_residual, grid_for(lv->n, kBlk), kBlk, 0, s, 
             lv->n, lv->A.off.p, lv->A.col.p, lv->A.val.p, x, f, r);
@@ -216,11 +231,19 @@ void level_residual(const ocmg_level *lv, const double *x, const double *f,
 void level_ne_jacobi(const ocmg_level *lv, double tau, double *x, double *r,
                      double *scratch, cudaStream_t s) {
     if (lv->kind == kP1) {
-        const int64_t N = (int64_t)lv->n1 * lv->n1;
-        OCMG_LAUNCH(k_p1_ne_p, grid_for(N, kBlk), kBlk, 0, s, lv->n1, lv->tables.p, tau,
-                                                     r, scratch);
-        OCMG_LAUNCH(k_p1_ne_apply, grid_for(N, kBlk), kBlk, 0, s, lv->n1, lv->tables.p,
-                                                         scratch, x, r);
+        const dim3 g = p1_interior_grid(lv->n1), b(kTX, kTY);
+        const int64_t nring = p1_ring_count(lv->n1, kRing);
+        P1JacCoef C;
+        for (int t = 0; t < 28; ++t) C.w[t] = lv->cW.c[t];
+        C.l[0] = lv->cL[0];
+        C.l[1] = lv->cL[1];
+        C.tau = tau;
+        OCMG_LAUNCH(k_p1_ne_p_int, g, b, 0, s, lv->n1, C, r, scratch);
+        OCMG_LAUNCH(k_p1_ne_p_ring, grid_for(nring, kBlk), kBlk, 0, s, lv->n1,
+                    lv->tables.p, tau, r, scratch);
+        OCMG_LAUNCH(k_p1_ne_apply_int, g, b, 0, s, lv->n1, lv->cA, scratch, x, r);
+        OCMG_LAUNCH(k_p1_ne_apply_ring, grid_for(nring, kBlk), kBlk, 0, s, lv->n1,
+                    lv->tables.p, scratch, x, r);
     } else {
         OCMG_LAUNCH(k_csr_ne_p, grid_for(lv->n, kBlk), kBlk, 0, s, 
             lv->n, lv->A.off.p, lv->A.col.p, lv->W.p, lv->L.p, tau, r, scratch);
@@ -252,12 +275,20 @@ void level_ne_gs(const ocmg_level *lv, int mode, bool forward, double *x,
     if (lv->kind == kP1) {
         const int n1 = lv->n1;
         if (mode == OCMG_GS_MULTICOLOUR) {
-            const int64_t work = (int64_t)((n1 + 6) / 7) * n1;
-            for (int b = 0; b < 14; ++b) {
-                const int c = forward ? b : 13 - b;
-                OCMG_LAUNCH(k_p1_gs_colour, grid_for(work, kBlk), kBlk, 0, s, 
-                    n1, lv->tables.p, c, x, r);
-            }
+            McsParams P{};
+            P.n1 = n1;
+            P.nstrips = lv->mc.nstrips;
+            P.base = lv->mc.base;
+            P.rem = lv->mc.rem;
+            P.forward = forward ? 1 : 0;
+            std::copy(lv->mc_ci, lv->mc_ci + 58, &P.ci[0][0]);
+            P.C = lv->mc_coef.p;
+            P.rin = r;
+            P.rout = lv->mc_r.p;
+            P.x = x;
+            OCMG_LAUNCH(k_p1_mc_sweep, lv->mc.grid, mcs::NT, mcs::SMEM, s, P);
+            OCMG_CUDA(cudaMemcpyAsync(r, lv->mc_r.p, sizeof(double) * lv->n,
+                                      cudaMemcpyDeviceToDevice, s));
         } else if (mode == OCMG_GS_WAVEFRONT && lv->wf.ready()) {
             lv->wf.sweep(forward, x, r, s);
         } else {
@@ -388,8 +419,10 @@ void coarse_solve(const ocmg_coarse *c, const double *rhs, double *x,
 void do_restrict(const ocmg_transfer *t, const double *rf, double *rc,
                  cudaStream_t s) {
     if (t->kind == kP1) {
-        OCMG_LAUNCH(k_p1_restrict, grid_for((int64_t)t->nc1 * t->nc1, kBlk), kBlk, 0, s, 
-            t->nc1, t->n_fields, rf, rc);
+        const int m = t->nc1;
+        const dim3 g((m + kTX - 1) / kTX, (m + kTY * kRPT - 1) / (kTY * kRPT));
+        OCMG_LAUNCH(k_p1_restrict_tiled, g, dim3(kTX, kTY), 0, s, t->nc1, t->n_fields,
+                    rf, rc);
     } else {
         OCMG_LAUNCH(k_csr_spmv, grid_for(t->nc, kBlk), kBlk, 0, s, 
             t->nc, t->R.off.p, t->R.col.p, t->R.val.p, rf, rc);
@@ -401,8 +434,10 @@ void do_prolong_add(const ocmg_transfer *t, const double *c, double *xf,
                     cudaStream_t s) {
     if (t->kind == kP1) {
         const int nf1 = 2 * t->nc1 - 1;
-        OCMG_LAUNCH(k_p1_prolong_add, grid_for((int64_t)nf1 * nf1, kBlk), kBlk, 0, s, 
-            t->nc1, t->n_fields, c, xf);
+        const int m = t->nc1;
+        const dim3 g((nf1 + kTX - 1) / kTX, (m + kTY * kRPT - 1) / (kTY * kRPT));
+        OCMG_LAUNCH(k_p1_prolong_add_tiled, g, dim3(kTX, kTY), 0, s, t->nc1,
+                    t->n_fields, c, xf);
     } else {
         OCMG_LAUNCH(k_csr_spmv_add, grid_for(t->nf, kBlk), kBlk, 0, s, 
             t->nf, t->P.off.p, t->P.col.p, t->P.val.p, c, xf);
@@ -570,7 +605,39 @@ int ocmg_level_create_p1(int k, double alpha, const double *tables,
         lv->nnz = 4 * pairs;
         lv->field_off = {0, N, 2 * N};
         lv->tables.upload(tables, n_tables);
+        for (int t = 0; t < 28; ++t) {
+            lv->cA.c[t] = tables[kP1OffA + 24 * 28 + t];
+            lv->cW.c[t] = tables[kP1OffW + 24 * 28 + t];
+        }
+        lv->cL[0] = tables[kP1OffL + 24 * 2];
+        lv->cL[1] = tables[kP1OffL + 24 * 2 + 1];
         lv->wf.init(lv->k, lv->n1, lv->tables.p, lv->tables.p + kP1TableDoubles);
+        {
+            static bool attr = false;
+            if (!attr) {
+                OCMG_CUDA(cudaFuncSetAttribute(k_p1_mc_sweep,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               mcs::SMEM));
+                attr = true;
+            }
+            int dev = 0, sms = 148;
+            OCMG_CUDA(cudaGetDevice(&dev));
+            OCMG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            lv->mc = mcs_plan(lv->n1, sms);
+            lv->mc_r.alloc(lv->n);
+            std::vector<double> C(49 * 2 * 29);
+            for (int c = 0; c < 49; ++c)
+                for (int f = 0; f < 2; ++f) {
+                    double *o = C.data() + (c * 2 + f) * 29;
+                    for (int e = 0; e < 14; ++e) {
+                        o[e] = tables[kP1OffW + c * 28 + f * 14 + e];
+                        o[14 + e] = tables[kP1OffA + c * 28 + f * 14 + e];
+                    }
+                    o[28] = 1.0 / tables[kP1OffND + c * 2 + f];
+                }
+            lv->mc_coef.upload(C.data(), (int64_t)C.size());
+            std::copy(C.data() + 24 * 58, C.data() + 25 * 58, lv->mc_ci);
+        }
         lv->partial.alloc(kRedGrid);
         lv->scal.alloc(8);
         *out = lv.release();
@@ -867,5 +934,23 @@ extern "C" int ocmg__debug_wf_prof(const ocmg_level *lv, unsigned long long *out
             OCMG_CUDA(cudaMemcpy(out, lv->wf.prof.p,
                                  lv->wf.prof.n * sizeof(unsigned long long),
                                  cudaMemcpyDeviceToHost));
+    });
+}
+
+// internal: the multicolour sweep as 14 colour passes (one launch per
+// colour, in place) -- the reference form the one-launch kernel must match
+extern "C" int ocmg__debug_mc_passes(const ocmg_level *lv, int forward, double *x,
+                                     double *r, void *stream) {
+    return guarded([&] {
+        OCMG_REQUIRE(lv && lv->kind == kP1 && x && r, "structured P1 level only");
+        const int n1 = lv->n1;
+        const int64_t work = (int64_t)((n1 + 6) / 7) * n1;
+        cudaStream_t s = as_stream(stream);
+        for (int b = 0; b < 14; ++b) {
+            const int c = forward ? b : 13 - b;
+            OCMG_LAUNCH(k_p1_gs_colour, grid_for(work, kBlk), kBlk, 0, s, n1,
+                        lv->tables.p, c, x, r);
+        }
+        OCMG_LAUNCH_CHECK();
     });
 }

@@ -199,6 +199,37 @@ __global__ void k_p1_gs_level(int n1, const double *__restrict__ T, int t,
     p1_gs_unknown(field, ix, iy, n1, T, x, r);
 }
 
+// One unknown of the multicolour sweep (same formula as mcs::node_update in
+// ocmg_p1_mc.cuh): two FMA chains, times 1/n_diag, r updated by FMA; absent
+// neighbours are skipped (their coefficients are 0 there).
+__device__ __forceinline__ void p1_mc_unknown(int field, int ix, int iy, int n1,
+                                              const double *__restrict__ T,
+                                              double *__restrict__ x,
+                                              double *__restrict__ r) {
+    const int64_t N = (int64_t)n1 * n1;
+    const P1Node q = p1_node(ix, iy, n1);
+    const double *W = T + kP1OffW + q.c * 28 + 14 * field;
+    const double *A = T + kP1OffA + q.c * 28 + 14 * field;
+    const double rnd = __drcp_rn(__ldg(T + kP1OffND + q.c * 2 + field));
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int d = 0; d < 7; ++d)
+        if (q.ex[d]) {
+            s0 = __fma_rn(__ldg(W + d), r[q.nb[d]], s0);
+            s1 = __fma_rn(__ldg(W + 7 + d), r[N + q.nb[d]], s1);
+        }
+    const double p = __dmul_rn(__dadd_rn(s0, s1), rnd);
+    const int64_t i = field * N + q.v;
+    x[i] = __dadd_rn(x[i], p);
+#pragma unroll
+    for (int d = 0; d < 7; ++d)
+        if (q.ex[d]) {
+            const int64_t j = q.nb[d];
+            r[j] = __fma_rn(-__ldg(A + d), p, r[j]);
+            r[N + j] = __fma_rn(-__ldg(A + 7 + d), p, r[N + j]);
+        }
+}
+
 // One colour of the distance-2 multicolour order: colour c in 0..13 is
 // field c/7 and (ix + 2 iy) mod 7 == c % 7.  Same-colour unknowns are at
 // graph distance >= 3 (no 19-point offset satisfies dx + 2 dy = 0 mod 7).
@@ -213,7 +244,7 @@ __global__ void k_p1_gs_colour(int n1, const double *__restrict__ T,
     const int cc = colour % 7;
     const int ix = ((cc - 2 * iy) % 7 + 7) % 7 + 7 * jj;
     if (ix >= n1) return;
-    p1_gs_unknown(colour / 7, ix, iy, n1, T, x, r);
+    p1_mc_unknown(colour / 7, ix, iy, n1, T, x, r);
 }
 
 // partial[b] = sum over a grid-strided slice of L_i x_i^2 (both fields)

@@ -17,6 +17,7 @@ if not torch.cuda.is_available():
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 import paper_1502_03917_b200 as P  # noqa: E402
+from paper_1502_03917_b200 import _lib  # noqa: E402
 
 
 def dev(a):
@@ -189,6 +190,33 @@ def test_ne_gs_multicolour_matches_permuted_oracle(prob, k, alpha):
     inv[perm] = np.arange(perm.size)
     assert rel(host(xd), xo[inv]) < 1e-13
     assert rel(host(rd), ro[inv]) < 1e-10
+
+
+@pytest.mark.parametrize("k", [3, 4, 6, 8, 10, 12])
+@pytest.mark.parametrize("forward", [True, False])
+def test_multicolour_one_launch_matches_colour_passes(k, forward):
+    """The pipelined one-launch multicolour sweep (strip tiles with halo,
+    all 14 colours in flight) is bit-identical to 14 in-place colour passes."""
+    import ctypes
+    dsys = P.build_poisson_system(k, 1e-6)
+    g = torch.Generator(device="cuda").manual_seed(11 + k)
+    x = torch.rand(dsys.n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    r = torch.rand(dsys.n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    x2, r2 = x.clone(), r.clone()
+    st = P.make_smoother(dsys, "lsgs", gs_mode="multicolour")
+    for _ in range(2):
+        if forward:
+            st.sweep(x, r)
+        else:
+            P.smoothers.lsgs_sweep(st, x, r, order="backward")
+        fn = _lib.load().ocmg__debug_mc_passes
+        fn.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+                       ctypes.c_void_p, ctypes.c_void_p]
+        _lib.check(fn(dsys.handle, int(forward), _lib.dptr(x2), _lib.dptr(r2),
+                      _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    assert torch.equal(x, x2)
+    assert torch.equal(r, r2)
 
 
 @pytest.mark.parametrize("prob,kc", [("poisson", 1), ("poisson", 4),
