@@ -3,9 +3,10 @@
 
 Headline workload (BASELINE.json configs[2], the north_star target): level 12
 (4097 x 4097 P1 nodes, 33,570,818 unknowns, fp64, alpha = 1e-6), one step =
-one forward NE-GS sweep in the reference's order (wavefront mode) over the
-finest level, x and r resident in HBM (537 MB > the 126 MB L2, so no flush
-is needed between steps).  Also reported: every hot kernel of the cycle on
+one forward NE-GS sweep over the finest level through the public sweep call
+(default: distance-2 multicolour mode; --mode wavefront = the reference's
+exact order, also reported under "modes"), x and r resident in HBM (537 MB >
+the 126 MB L2, so no flush is needed between steps).  Also reported: every hot kernel of the cycle on
 the same level, the time to 1e-8 of a multigrid solve, the end-to-end sweep
 through the public API with host buffers, the CPU oracle on the host, and
 the clocks seen during the timed region.
@@ -35,7 +36,10 @@ METRIC = ("fp64 DOF-updates/s per NE-GS sweep; multigrid time to 1e-8 rel. "
           "residual")
 UNIT = "DOF-updates/s"
 # algorithmic HBM bytes per unknown
-BYTES = {"ne_gs": 32, "ne_jacobi": 56, "residual": 24, "restrict": 10,
+# (x, r in and out for a sweep; x, f in and r out for the residual; fine in
+# plus coarse out per fine unknown for restriction; fine x in/out plus
+# coarse in for prolongation)
+BYTES = {"ne_gs": 32, "ne_jacobi": 32, "residual": 24, "restrict": 10,
          "prolong": 18}
 
 
@@ -190,6 +194,7 @@ def run_reference_arm(args, ws, rank):
 
 def time_events(fn, iters, stream):
     import torch
+    fn()  # warm (first calls allocate scratch / build plans)
     start = torch.cuda.Event(enable_timing=True)
     stop = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -257,6 +262,7 @@ def solve_timing(level, alpha, cycle, coarsest, mode, sine):
                       f"NE-GS[{mode}] coarsest L{coarsest}"
                       + (" y_D=U+sin*sin" if sine else ""),
             "cycles": len(hist), "final_rel_residual": hist[-1],
+            "convergence_factor": float(hist[-1] ** (1.0 / len(hist))),
             "seconds": t, "setup_seconds": t_setup}
 
 
@@ -351,11 +357,21 @@ def run_gpu_arm(args, ws, rank, local):
             tr = system_transfer(coarse, dsys)
             result["kernels"] = kernel_table(dsys, coarse, tr, x, r, f,
                                              stream, args.kernel_iters, hbm)
-            result["solve"] = [solve_timing(10, 1e-4, "v", 2, args.mode,
-                                            False)]
-            if args.solve_l12:
-                result["solve"].append(solve_timing(
-                    args.level, args.alpha, "w", 1, args.mode, True))
+            other = "wavefront" if args.mode == "multicolour" else "multicolour"
+            result["modes"] = {args.mode: {"dof_per_s": value,
+                                           "ms": t_step * 1e3}}
+            st_o = P.make_smoother(dsys, "lsgs", gs_mode=other)
+            st_o.sweep(x, r)
+            t_o = time_events(lambda: st_o.sweep(x, r), 3, stream)
+            result["modes"][other] = {"dof_per_s": n / t_o, "ms": t_o * 1e3}
+            result["solve"] = [solve_timing(10, 1e-4, "v", 2, m, False)
+                               for m in ("multicolour", "wavefront")]
+            if not args.no_solve_l12:
+                modes = ["multicolour"] + (["wavefront"]
+                                           if args.solve_l12_wavefront else [])
+                for m in modes:
+                    result["solve"].append(solve_timing(
+                        args.level, args.alpha, "w", 3, m, True))
         if ws == 1 and not args.no_cpu:
             v, dt, ncpu = cpu_sweep_rate(args.cpu_level, args.cpu_sweeps,
                                          args.alpha)
@@ -378,12 +394,14 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--level", type=int, default=12)
     ap.add_argument("--alpha", type=float, default=1e-6)
-    ap.add_argument("--mode", default="wavefront",
+    ap.add_argument("--mode", default="multicolour",
                     choices=["wavefront", "reference", "multicolour"])
     ap.add_argument("--quick", action="store_true",
                     help="headline only (no kernel table / solves)")
-    ap.add_argument("--solve-l12", action="store_true",
-                    help="also time the config-3 W-cycle solve at L12")
+    ap.add_argument("--no-solve-l12", action="store_true",
+                    help="skip the config-3 W-cycle solves at L12")
+    ap.add_argument("--solve-l12-wavefront", action="store_true",
+                    help="also time the exact-order (wavefront) W-cycle at L12")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-level", type=int, default=10)
     ap.add_argument("--cpu-sweeps", type=int, default=10)

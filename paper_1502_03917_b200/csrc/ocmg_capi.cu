@@ -14,6 +14,7 @@
 #include "ocmg_p1.cuh"
 #include "ocmg_p1_tiled.cuh"
 #include "ocmg_p1_mc.cuh"
+#include "ocmg_p1_mc_small.cuh"
 #include "ocmg_wavefront.cuh"
 
 using namespace ocmg;
@@ -40,6 +41,7 @@ enum LevelKind { kCsr = 0, kP1 = 1 };
 struct Schedule {  // rows bucketed by dependency level (or colour)
     DevBuf<int32_t> rows;
     std::vector<int64_t> off;
+    DevBuf<int64_t> doff;  // device copy of off (one-CTA sweep)
 };
 
 }  // namespace
@@ -63,6 +65,9 @@ struct ocmg_level {
     P1Coef28 cA{}, cW{};  // class-(3,3) A and row_scaled rows (tiled kernels)
     double cL[2] = {0.0, 0.0};
     P1Wavefront wf;
+    int mc_tier = 2;          // 0 one-CTA, 1 cooperative, 2 pipelined strips
+    int mc_grid = 0;          // tier-1 CTAs
+    DevBuf<unsigned> mc_bar;  // tier-1 grid barrier
     McsPlan mc;               // one-launch multicolour sweep geometry
     DevBuf<double> mc_r;      // its out-of-place residual
     DevBuf<double> mc_coef;   // [49][2][29] W row, A row, n_diag
@@ -135,6 +140,7 @@ Schedule build_schedule(int64_t n, const int64_t *off, const int64_t *col,
         rows[fill[lev[i]]++] = (int32_t)i;
     }
     S.rows.upload(rows);
+    S.doff.upload(S.off);
     return S;
 }
 
@@ -166,6 +172,7 @@ Schedule build_colouring(int64_t n, const int64_t *off, const int64_t *col) {
     std::vector<int64_t> fill(S.off.begin(), S.off.end() - 1);
     for (int64_t i = 0; i < n; ++i) rows[fill[colour[i]]++] = (int32_t)i;
     S.rows.upload(rows);
+    S.doff.upload(S.off);
     return S;
 }
 
@@ -256,6 +263,14 @@ void level_ne_jacobi(const ocmg_level *lv, double tau, double *x, double *r,
 void run_schedule(const ocmg_level *lv, const Schedule &S, bool reverse,
                   double *x, double *r, cudaStream_t s) {
     const int64_t nb = (int64_t)S.off.size() - 1;
+    if (lv->n <= kCsrSmallN) {
+        // small level: every group in one CTA, __syncthreads between groups
+        OCMG_LAUNCH(k_csr_gs_sched_small, 1, 1024, 0, s, (int)nb, S.doff.p,
+                    S.rows.p, reverse ? 1 : 0, lv->A.off.p, lv->A.col.p, lv->A.val.p,
+                    lv->W.p, lv->ndiag.p, x, r);
+        OCMG_LAUNCH_CHECK();
+        return;
+    }
     for (int64_t b = 0; b < nb; ++b) {
         const int64_t l = reverse ? nb - 1 - b : b;
         const int64_t lo = S.off[l], cnt = S.off[l + 1] - lo;
@@ -268,6 +283,42 @@ void run_schedule(const ocmg_level *lv, const Schedule &S, bool reverse,
     OCMG_LAUNCH_CHECK();
 }
 
+// one multicolour sweep.  Tiers 0/1 update r in place (returns false);
+// tier 2 reads r and writes the new residual to rout (returns true).
+bool p1_mc_sweep(const ocmg_level *lv, bool forward, double *x, double *r,
+                 double *rout, cudaStream_t s) {
+    if (lv->mc_tier == 0) {
+        OCMG_LAUNCH(k_p1_mc_small, 1, 1024, mc_small_smem(lv->n1), s, lv->n1,
+                    forward ? 1 : 0, lv->mc_coef.p, x, r);
+        OCMG_LAUNCH_CHECK();
+        return false;
+    }
+    if (lv->mc_tier == 1) {
+        int n1 = lv->n1, fw = forward ? 1 : 0;
+        const double *T = lv->tables.p;
+        unsigned *bar = lv->mc_bar.p;
+        void *args[] = {&n1, &fw, &T, &x, &r, &bar};
+        launch_counter().fetch_add(1, std::memory_order_relaxed);
+        OCMG_CUDA(cudaLaunchCooperativeKernel((const void *)k_p1_mc_grid,
+                                              dim3(lv->mc_grid), dim3(256), args, 0, s));
+        return false;
+    }
+    McsParams P{};
+    P.n1 = lv->n1;
+    P.nstrips = lv->mc.nstrips;
+    P.base = lv->mc.base;
+    P.rem = lv->mc.rem;
+    P.forward = forward ? 1 : 0;
+    std::copy(lv->mc_ci, lv->mc_ci + 58, &P.ci[0][0]);
+    P.C = lv->mc_coef.p;
+    P.rin = r;
+    P.rout = rout;
+    P.x = x;
+    OCMG_LAUNCH(k_p1_mc_sweep, lv->mc.grid, mcs::NT, mcs::SMEM, s, P);
+    OCMG_LAUNCH_CHECK();
+    return true;
+}
+
 void level_ne_gs(const ocmg_level *lv, int mode, bool forward, double *x,
                  double *r, cudaStream_t s) {
     OCMG_REQUIRE(mode >= OCMG_GS_REFERENCE && mode <= OCMG_GS_MULTICOLOUR,
@@ -275,20 +326,9 @@ void level_ne_gs(const ocmg_level *lv, int mode, bool forward, double *x,
     if (lv->kind == kP1) {
         const int n1 = lv->n1;
         if (mode == OCMG_GS_MULTICOLOUR) {
-            McsParams P{};
-            P.n1 = n1;
-            P.nstrips = lv->mc.nstrips;
-            P.base = lv->mc.base;
-            P.rem = lv->mc.rem;
-            P.forward = forward ? 1 : 0;
-            std::copy(lv->mc_ci, lv->mc_ci + 58, &P.ci[0][0]);
-            P.C = lv->mc_coef.p;
-            P.rin = r;
-            P.rout = lv->mc_r.p;
-            P.x = x;
-            OCMG_LAUNCH(k_p1_mc_sweep, lv->mc.grid, mcs::NT, mcs::SMEM, s, P);
-            OCMG_CUDA(cudaMemcpyAsync(r, lv->mc_r.p, sizeof(double) * lv->n,
-                                      cudaMemcpyDeviceToDevice, s));
+            if (p1_mc_sweep(lv, forward, x, r, lv->mc_r.p, s))
+                OCMG_CUDA(cudaMemcpyAsync(r, lv->mc_r.p, sizeof(double) * lv->n,
+                                          cudaMemcpyDeviceToDevice, s));
         } else if (mode == OCMG_GS_WAVEFRONT && lv->wf.ready()) {
             lv->wf.sweep(forward, x, r, s);
         } else {
@@ -464,6 +504,29 @@ void smooth(ocmg_hierarchy *h, int hi, double *x, double *r, cudaStream_t s) {
     }
 }
 
+// nu smoothing steps; multicolour sweeps on structured levels ping-pong the
+// residual between r and the level scratch instead of copying it back
+void smooth_n(ocmg_hierarchy *h, int hi, int nu, double *x, double *r,
+              cudaStream_t s) {
+    ocmg_level *lv = h->levels[hi - 1];
+    const ocmg_cycle_config &c = h->cfg;
+    if (!(lv->kind == kP1 && c.gs_mode == OCMG_GS_MULTICOLOUR &&
+          c.smoother != OCMG_SMOOTHER_NORMAL)) {
+        for (int i = 0; i < nu; ++i) smooth(h, hi, x, r, s);
+        return;
+    }
+    double *buf[2] = {r, h->scratch[hi].p};
+    int cur = 0;
+    for (int i = 0; i < nu; ++i) {
+        const int nsw = c.smoother == OCMG_SMOOTHER_LSGS ? 1 : 2;
+        for (int k = 0; k < nsw; ++k)
+            if (p1_mc_sweep(lv, k == 0, x, buf[cur], buf[1 - cur], s)) cur = 1 - cur;
+    }
+    if (cur)
+        OCMG_CUDA(cudaMemcpyAsync(r, buf[1], sizeof(double) * lv->n,
+                                  cudaMemcpyDeviceToDevice, s));
+}
+
 void cycle_rec(ocmg_hierarchy *h, int hi, double *x, const double *rhs,
                cudaStream_t s) {
     if (hi == 0) {
@@ -474,7 +537,7 @@ void cycle_rec(ocmg_hierarchy *h, int hi, double *x, const double *rhs,
     ocmg_transfer *tr = h->transfers[hi - 1];
     double *r = h->r[hi].p;
     level_residual(lv, x, rhs, r, s);
-    for (int i = 0; i < h->cfg.nu_pre; ++i) smooth(h, hi, x, r, s);
+    smooth_n(h, hi, h->cfg.nu_pre, x, r, s);
     double *crhs = h->crhs[hi - 1].p, *corr = h->corr[hi - 1].p;
     do_restrict(tr, r, crhs, s);
     const int64_t nc = h->corr[hi - 1].n;
@@ -486,7 +549,7 @@ void cycle_rec(ocmg_hierarchy *h, int hi, double *x, const double *rhs,
     do_prolong_add(tr, corr, x, s);
     level_mean_project(lv, x, s);
     level_residual(lv, x, rhs, r, s);
-    for (int i = 0; i < h->cfg.nu_post; ++i) smooth(h, hi, x, r, s);
+    smooth_n(h, hi, h->cfg.nu_post, x, r, s);
 }
 
 // one cycle + projection + ||f - A x||^2 into h->scal[0]
@@ -624,7 +687,25 @@ int ocmg_level_create_p1(int k, double alpha, const double *tables,
             OCMG_CUDA(cudaGetDevice(&dev));
             OCMG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
             lv->mc = mcs_plan(lv->n1, sms);
-            lv->mc_r.alloc(lv->n);
+            static bool attr2 = false;
+            if (!attr2) {
+                OCMG_CUDA(cudaFuncSetAttribute(k_p1_mc_small,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               mc_small_smem(kMcSmallMaxN1)));
+                attr2 = true;
+            }
+            lv->mc_tier = lv->n1 <= kMcSmallMaxN1 ? 0 : lv->n1 <= kMcGridMaxN1 ? 1 : 2;
+            if (lv->mc_tier == 1) {
+                int occ = 0;
+                OCMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p1_mc_grid,
+                                                                        256, 0));
+                const int64_t work = (int64_t)((lv->n1 + 6) / 7) * lv->n1;
+                lv->mc_grid = (int)std::min<int64_t>((work + 255) / 256,
+                                                     (int64_t)std::max(1, occ) * sms);
+                lv->mc_bar.alloc(2);
+                OCMG_CUDA(cudaMemset(lv->mc_bar.p, 0, 2 * sizeof(unsigned)));
+            }
+            if (lv->mc_tier == 2) lv->mc_r.alloc(lv->n);
             std::vector<double> C(49 * 2 * 29);
             for (int c = 0; c < 49; ++c)
                 for (int f = 0; f < 2; ++f) {
@@ -823,7 +904,9 @@ int ocmg_hierarchy_create(int n_levels, ocmg_level *const *levels,
         }
         for (int hi = 1; hi <= n_levels; ++hi) {
             h->r[hi].alloc(sizes[hi]);
-            if (cfg->smoother == OCMG_SMOOTHER_NORMAL)
+            // NE-Jacobi update vector / multicolour ping-pong residual
+            if (cfg->smoother == OCMG_SMOOTHER_NORMAL ||
+                cfg->gs_mode == OCMG_GS_MULTICOLOUR)
                 h->scratch[hi].alloc(sizes[hi]);
         }
         for (int hi = 0; hi < n_levels; ++hi) {

@@ -104,6 +104,25 @@ __global__ void k_csr_ne_apply(int64_t n, const int64_t *__restrict__ off,
 // in `rows` are pairwise at graph distance >= 3, so their updates commute
 // and every r_j still receives its updates in index order.  A is symmetric
 // (checked at level creation), so column i of A is row i.
+__device__ __forceinline__ void csr_gs_row(int32_t i, const int64_t *__restrict__ off,
+                                           const int32_t *__restrict__ col,
+                                           const double *__restrict__ val,
+                                           const double *__restrict__ w,
+                                           const double *__restrict__ ndiag,
+                                           double *__restrict__ x,
+                                           double *__restrict__ r) {
+    const int64_t b = off[i], e = off[i + 1];
+    double q = 0.0;
+    for (int64_t t = b; t < e; ++t)
+        q = __dadd_rn(q, __dmul_rn(w[t], r[col[t]]));
+    const double p = __ddiv_rn(q, ndiag[i]);
+    x[i] = __dadd_rn(x[i], p);
+    for (int64_t t = b; t < e; ++t) {
+        const int32_t j = col[t];
+        r[j] = __dsub_rn(r[j], __dmul_rn(val[t], p));
+    }
+}
+
 __global__ void k_csr_gs_rows(int cnt, const int32_t *__restrict__ rows,
                               const int64_t *__restrict__ off,
                               const int32_t *__restrict__ col,
@@ -114,16 +133,29 @@ __global__ void k_csr_gs_rows(int cnt, const int32_t *__restrict__ rows,
                               double *__restrict__ r) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= cnt) return;
-    const int32_t i = rows[k];
-    const int64_t b = off[i], e = off[i + 1];
-    double q = 0.0;
-    for (int64_t t = b; t < e; ++t)
-        q = __dadd_rn(q, __dmul_rn(w[t], r[col[t]]));
-    const double p = __ddiv_rn(q, ndiag[i]);
-    x[i] = __dadd_rn(x[i], p);
-    for (int64_t t = b; t < e; ++t) {
-        const int32_t j = col[t];
-        r[j] = __dsub_rn(r[j], __dmul_rn(val[t], p));
+    csr_gs_row(rows[k], off, col, val, w, ndiag, x, r);
+}
+
+// Whole sweep of a small level in one CTA: the groups (dependency levels or
+// colours) in order, __syncthreads between them (one launch instead of one
+// per group -- the coarse levels of a W-cycle are visited thousands of times)
+constexpr int64_t kCsrSmallN = 8192;
+
+__global__ void __launch_bounds__(1024)
+    k_csr_gs_sched_small(int ngroups, const int64_t *__restrict__ goff,
+                         const int32_t *__restrict__ rows, int reverse,
+                         const int64_t *__restrict__ off,
+                         const int32_t *__restrict__ col,
+                         const double *__restrict__ val,
+                         const double *__restrict__ w,
+                         const double *__restrict__ ndiag,
+                         double *__restrict__ x, double *__restrict__ r) {
+    for (int g = 0; g < ngroups; ++g) {
+        const int l = reverse ? ngroups - 1 - g : g;
+        const int lo = (int)goff[l], hi = (int)goff[l + 1];
+        for (int k = lo + threadIdx.x; k < hi; k += blockDim.x)
+            csr_gs_row(rows[k], off, col, val, w, ndiag, x, r);
+        __syncthreads();
     }
 }
 

@@ -211,12 +211,18 @@ __device__ __forceinline__ void p1_mc_unknown(int field, int ix, int iy, int n1,
     const double *W = T + kP1OffW + q.c * 28 + 14 * field;
     const double *A = T + kP1OffA + q.c * 28 + 14 * field;
     const double rnd = __drcp_rn(__ldg(T + kP1OffND + q.c * 2 + field));
+    double v0[7], v1[7];
+#pragma unroll
+    for (int d = 0; d < 7; ++d) {
+        v0[d] = q.ex[d] ? __ldcg(r + q.nb[d]) : 0.0;
+        v1[d] = q.ex[d] ? __ldcg(r + N + q.nb[d]) : 0.0;
+    }
     double s0 = 0.0, s1 = 0.0;
 #pragma unroll
     for (int d = 0; d < 7; ++d)
         if (q.ex[d]) {
-            s0 = __fma_rn(__ldg(W + d), r[q.nb[d]], s0);
-            s1 = __fma_rn(__ldg(W + 7 + d), r[N + q.nb[d]], s1);
+            s0 = __fma_rn(__ldg(W + d), v0[d], s0);
+            s1 = __fma_rn(__ldg(W + 7 + d), v1[d], s1);
         }
     const double p = __dmul_rn(__dadd_rn(s0, s1), rnd);
     const int64_t i = field * N + q.v;
@@ -224,9 +230,8 @@ __device__ __forceinline__ void p1_mc_unknown(int field, int ix, int iy, int n1,
 #pragma unroll
     for (int d = 0; d < 7; ++d)
         if (q.ex[d]) {
-            const int64_t j = q.nb[d];
-            r[j] = __fma_rn(-__ldg(A + d), p, r[j]);
-            r[N + j] = __fma_rn(-__ldg(A + 7 + d), p, r[N + j]);
+            __stcg(r + q.nb[d], __fma_rn(-__ldg(A + d), p, v0[d]));
+            __stcg(r + N + q.nb[d], __fma_rn(-__ldg(A + 7 + d), p, v1[d]));
         }
 }
 

@@ -1,0 +1,110 @@
+// Multicolour NE-GS sweep for the small and middle levels of a cycle, where
+// the pipelined strip kernel (ocmg_p1_mc.cuh) would spend most of its steps
+// filling and draining.  Same order and arithmetic (p1_mc_unknown /
+// mcs::node_update), so all three forms are bit-identical.
+//
+//   k <= 6  (n1 <= 65):  k_p1_mc_small -- one CTA, the whole residual in
+//                        shared memory (guard ring of zeros), 14 colour
+//                        phases separated by __syncthreads.
+//   7 <= k <= 9:         k_p1_mc_grid -- one cooperative launch, 14 colour
+//                        phases separated by a grid barrier, in place.
+#pragma once
+
+#include "ocmg_p1_mc.cuh"
+
+namespace ocmg {
+
+constexpr int kMcSmallMaxN1 = 65;
+constexpr int kMcGridMaxN1 = 513;
+
+__host__ __device__ constexpr int mc_small_smem(int n1) {
+    return (n1 + 2) * (n1 + 2) * 16;
+}
+
+__global__ void __launch_bounds__(1024)
+    k_p1_mc_small(int n1, int forward, const double *__restrict__ C,
+                  double *__restrict__ x, double *__restrict__ r) {
+    extern __shared__ double2 g[];  // [(n1+2)^2] (state, adjoint), zero guards
+    const int P = n1 + 2;
+    const int64_t N = (int64_t)n1 * n1;
+    for (int i = threadIdx.x; i < P * P; i += blockDim.x) {
+        const int gy = i / P, gx = i - gy * P;
+        const int ix = gx - 1, iy = gy - 1;
+        double2 v = make_double2(0.0, 0.0);
+        if (ix >= 0 && ix < n1 && iy >= 0 && iy < n1) {
+            const int64_t k = (int64_t)iy * n1 + ix;
+            v = make_double2(r[k], r[N + k]);
+        }
+        g[i] = v;
+    }
+    __syncthreads();
+    const int per_row = (n1 + 6) / 7;
+    const int count = per_row * n1;
+    for (int b = 0; b < 14; ++b) {
+        const int colour = forward ? b : 13 - b;
+        const int field = colour / 7, cm = colour % 7;
+        for (int k = threadIdx.x; k < count; k += blockDim.x) {
+            const int iy = k / per_row, jj = k - iy * per_row;
+            const int ix = ((cm - 2 * iy) % 7 + 7) % 7 + 7 * jj;
+            if (ix >= n1) continue;
+            const int c = (iy + 1) * P + ix + 1;
+            double2 *const adr[7] = {g + c - P - 1, g + c - P, g + c - 1, g + c,
+                                     g + c + 1,     g + c + P, g + c + P + 1};
+            const int cls = 7 * p1_axis_class(iy, n1) + p1_axis_class(ix, n1);
+            const double p = mcs::node_update<false>(adr, nullptr, nullptr, 0.0,
+                                                     C + (cls * 2 + field) * 29);
+            const int64_t xi = field * N + (int64_t)iy * n1 + ix;
+            x[xi] = __dadd_rn(x[xi], p);
+        }
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < P * P; i += blockDim.x) {
+        const int gy = i / P, gx = i - gy * P;
+        const int ix = gx - 1, iy = gy - 1;
+        if (ix >= 0 && ix < n1 && iy >= 0 && iy < n1) {
+            const int64_t k = (int64_t)iy * n1 + ix;
+            r[k] = g[i].x;
+            r[N + k] = g[i].y;
+        }
+    }
+}
+
+// sense-counting grid barrier for a cooperative launch (all CTAs resident)
+__device__ __forceinline__ void mc_grid_barrier(unsigned *count, unsigned *gen,
+                                                unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned g0 = *(volatile unsigned *)gen;
+        __threadfence();
+        if (atomicAdd(count, 1u) == nblocks - 1) {
+            *(volatile unsigned *)count = 0u;
+            __threadfence();
+            atomicAdd(gen, 1u);
+        } else {
+            while (*(volatile unsigned *)gen == g0) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(256)
+    k_p1_mc_grid(int n1, int forward, const double *__restrict__ T,
+                 double *__restrict__ x, double *__restrict__ r, unsigned *bar) {
+    const int per_row = (n1 + 6) / 7;
+    const int64_t count = (int64_t)per_row * n1;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int b = 0; b < 14; ++b) {
+        const int colour = forward ? b : 13 - b;
+        const int cm = colour % 7;
+        for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < count;
+             k += stride) {
+            const int iy = (int)(k / per_row), jj = (int)(k - (int64_t)iy * per_row);
+            const int ix = ((cm - 2 * iy) % 7 + 7) % 7 + 7 * jj;
+            if (ix < n1) p1_mc_unknown(colour / 7, ix, iy, n1, T, x, r);
+        }
+        if (b < 13) mc_grid_barrier(bar, bar + 1, gridDim.x);
+    }
+}
+
+}  // namespace ocmg
