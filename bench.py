@@ -36,10 +36,11 @@ METRIC = ("fp64 DOF-updates/s per NE-GS sweep; multigrid time to 1e-8 rel. "
           "residual")
 UNIT = "DOF-updates/s"
 # algorithmic HBM bytes per unknown
-# (x, r in and out for a sweep; x, f in and r out for the residual; fine in
-# plus coarse out per fine unknown for restriction; fine x in/out plus
-# coarse in for prolongation)
-BYTES = {"ne_gs": 32, "ne_jacobi": 32, "residual": 24, "restrict": 10,
+# (x, r in and out for an NE-GS sweep; the two NE-Jacobi
+# halves 16 + 40; x, f in and r out for the residual; fine in plus coarse out
+# per fine unknown for restriction; fine x in/out plus coarse in for
+# prolongation)
+BYTES = {"ne_gs": 32, "ne_jacobi": 56, "residual": 24, "restrict": 10,
          "prolong": 18}
 
 
@@ -284,8 +285,16 @@ def run_gpu_arm(args, ws, rank, local):
     st = P.make_smoother(dsys, "lsgs", gs_mode=args.mode)
     stream = torch.cuda.current_stream()
 
-    for _ in range(args.warmup):
-        st.sweep(x, r)
+    # the driver's form of a sweep: residual ping-pong between r and r2
+    from paper_1502_03917_b200.smoothers import lsgs_sweep_into
+    r2 = torch.empty_like(r)
+    bufs = [r, r2]
+
+    def step(i):
+        lsgs_sweep_into(st, x, bufs[i % 2], bufs[(i + 1) % 2])
+
+    for i in range(args.warmup + (args.warmup % 2)):
+        step(i)
     torch.cuda.synchronize()
     barrier(ws)
 
@@ -297,13 +306,15 @@ def run_gpu_arm(args, ws, rank, local):
         barrier(ws)
         torch.cuda.synchronize()
         start.record(stream)
-        for _ in range(args.steps):
-            st.sweep(x, r)
+        for i in range(args.steps):
+            step(i)
         stop.record(stream)
         stop.synchronize()
         launches = _lib.launch_count() - launches0
         barrier(ws)
     t_step = start.elapsed_time(stop) / args.steps / 1e3
+    if args.steps % 2:
+        r.copy_(r2)  # the current residual back in r
     t_step = max_over_ranks(t_step, ws, device)
     value = ws * n / t_step
 
@@ -339,6 +350,9 @@ def run_gpu_arm(args, ws, rank, local):
             "config": {"workload": f"poisson_control_L{args.level}_ne_gs_sweep",
                        "unknowns": n, "alpha": args.alpha,
                        "gs_mode": args.mode,
+                       "step": "one forward NE-GS sweep of the finest level "
+                               "(ocmg_ne_gs_sweep_into: residual ping-pong "
+                               "between two buffers, as in the cycle driver)",
                        "l2": "inputs larger than L2 (x+r 2x268 MB), no flush",
                        "parallelism": f"replicas x{ws}"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm,

@@ -115,6 +115,15 @@ int ocmg_ne_jacobi_sweep(const ocmg_level *lv, double tau, double *x,
 int ocmg_ne_gs_sweep(const ocmg_level *lv, int mode, int forward, double *x,
                      double *r, void *stream, int64_t *ops);
 
+/* The same sweep with the residual out of place: reads r_in, leaves the new
+ * residual in r_out (r_in may be overwritten).  This is the form the cycle
+ * driver runs (ping-pong buffers, no copy-back) for the multicolour mode on
+ * structured levels; other modes/levels copy r_in to r_out and sweep there.
+ * Not a reference entry point: a B200 addition next to ocmg_ne_gs_sweep. */
+int ocmg_ne_gs_sweep_into(const ocmg_level *lv, int mode, int forward, double *x,
+                          double *r_in, double *r_out, void *stream,
+                          int64_t *ops);
+
 /* Constant-mode removal of the pressure fields (pressure_mean_projection,
  * assembly.py:381-388); no-op for Poisson. */
 int ocmg_mean_project(const ocmg_level *lv, double *x, void *stream);

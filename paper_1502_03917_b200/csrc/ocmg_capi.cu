@@ -760,6 +760,24 @@ int ocmg_ne_gs_sweep(const ocmg_level *lv, int mode, int forward, double *x,
     });
 }
 
+int ocmg_ne_gs_sweep_into(const ocmg_level *lv, int mode, int forward, double *x,
+                          double *r_in, double *r_out, void *stream, int64_t *ops) {
+    return guarded([&] {
+        OCMG_REQUIRE(lv && x && r_in && r_out, "null argument");
+        OCMG_REQUIRE(r_in != r_out, "r_in and r_out must differ");
+        cudaStream_t s = as_stream(stream);
+        if (!(lv->kind == kP1 && mode == OCMG_GS_MULTICOLOUR &&
+              p1_mc_sweep(lv, forward != 0, x, r_in, r_out, s))) {
+            // in-place forms: sweep r_in, then hand it over
+            if (!(lv->kind == kP1 && mode == OCMG_GS_MULTICOLOUR))
+                level_ne_gs(lv, mode, forward != 0, x, r_in, s);
+            OCMG_CUDA(cudaMemcpyAsync(r_out, r_in, sizeof(double) * lv->n,
+                                      cudaMemcpyDeviceToDevice, s));
+        }
+        if (ops) *ops = 2 * lv->nnz;
+    });
+}
+
 int ocmg_mean_project(const ocmg_level *lv, double *x, void *stream) {
     return guarded([&] {
         OCMG_REQUIRE(lv && x, "null argument");

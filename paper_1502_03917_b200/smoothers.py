@@ -150,6 +150,25 @@ def lsgs_sweep(state, x, r, order="forward"):
     return x, r
 
 
+def lsgs_sweep_into(state, x, r_in, r_out, order="forward"):
+    """The NE-GS sweep with the residual out of place (device tensors only):
+    r_out receives the new residual, r_in may be overwritten.  The cycle
+    driver's form for multicolour levels (no copy-back); B200 addition."""
+    if order not in ("forward", "backward"):
+        raise ValueError("order must be 'forward' or 'backward'")
+    n = state.system.n
+    for t in (x, r_in, r_out):
+        if not (hasattr(t, "is_cuda") and t.is_cuda and t.numel() == n):
+            raise ValueError(f"expected CUDA tensors of length {n}")
+    ops = ctypes.c_int64()
+    _lib.call("ocmg_ne_gs_sweep_into", state.system.handle,
+              _lib.GS_MODES[state.gs_mode], 1 if order == "forward" else 0,
+              _lib.dptr(x), _lib.dptr(r_in), _lib.dptr(r_out),
+              _lib.stream_ptr(), ctypes.byref(ops))
+    state.op_count += ops.value
+    return x, r_out
+
+
 def slsgs_sweep(state, x, r):
     """Forward then backward NE-GS (smoothers.py:281-285)."""
     lsgs_sweep(state, x, r, order="forward")

@@ -219,6 +219,22 @@ def test_multicolour_one_launch_matches_colour_passes(k, forward):
     assert torch.equal(r, r2)
 
 
+@pytest.mark.parametrize("k", [4, 8, 10])
+@pytest.mark.parametrize("mode", ["multicolour", "wavefront"])
+def test_sweep_into_matches_in_place(k, mode):
+    dsys = P.build_poisson_system(k, 1e-4)
+    g = torch.Generator(device="cuda").manual_seed(3 + k)
+    x = torch.rand(dsys.n, dtype=torch.float64, device="cuda", generator=g)
+    r = torch.rand(dsys.n, dtype=torch.float64, device="cuda", generator=g)
+    x2, ra, rb = x.clone(), r.clone(), torch.empty_like(r)
+    st = P.make_smoother(dsys, "lsgs", gs_mode=mode)
+    st.sweep(x, r)
+    P.smoothers.lsgs_sweep_into(st, x2, ra, rb)
+    torch.cuda.synchronize()
+    assert torch.equal(x, x2)
+    assert torch.equal(r, rb)
+
+
 @pytest.mark.parametrize("prob,kc", [("poisson", 1), ("poisson", 4),
                                      ("stokes", 1), ("stokes", 3)])
 def test_transfers_bitwise(prob, kc):
