@@ -151,6 +151,16 @@ def test_device_path_has_no_cpu_fallback():
         P.build_poisson_system(4, 1e-6)
 
 
+def test_package_does_not_import_oracle():
+    """The oracle is test infrastructure: the product never loads it."""
+    import subprocess
+    import sys
+    code = ("import sys, paper_1502_03917_b200; "
+            "assert not any(m == 'oracle' or m.startswith('oracle.') "
+            "for m in sys.modules), 'oracle imported'")
+    subprocess.run([sys.executable, "-c", code], check=True, cwd=ROOT)
+
+
 def test_config_validation():
     import paper_1502_03917_b200 as P
     with pytest.raises(ValueError):
