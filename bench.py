@@ -267,6 +267,99 @@ def solve_timing(level, alpha, cycle, coarsest, mode, sine):
             "seconds": t, "setup_seconds": t_setup}
 
 
+def run_strip_arm(args, ws, rank, local):
+    """--partition strips (N > 1): ONE L12 system strip-partitioned over the
+    ranks (strong scaling).  A step is the ghost exchange (torch.distributed
+    P2P over NCCL) plus one multicolour strip sweep per rank
+    (paper_1502_03917_b200.strips); time = max over ranks."""
+    import torch
+
+    import paper_1502_03917_b200 as P
+    from paper_1502_03917_b200 import _lib
+    from paper_1502_03917_b200.strips import (StripPartition, exchange_ghosts,
+                                              strip_sweep)
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    hbm, peak_kind = peaks()
+    dsys = P.build_poisson_system(args.level, args.alpha)
+    n, n1 = dsys.n, 2 ** args.level + 1
+    part = StripPartition(n1, ws, rank)
+    g = torch.Generator(device=device).manual_seed(1234)  # same on all ranks
+    x = torch.rand(n, dtype=torch.float64, device=device, generator=g) * 2 - 1
+    f = torch.rand(n, dtype=torch.float64, device=device, generator=g) * 2 - 1
+    r = dsys.residual(x, f)
+    xo = part.scatter_own(x)
+    rs = [part.scatter(r), torch.empty((2, part.slab_rows, n1),
+                                       dtype=torch.float64, device=device)]
+    del x, f, r
+    stream = torch.cuda.current_stream()
+
+    def step(i):
+        cur = rs[i % 2]
+        exchange_ghosts(cur, part)
+        strip_sweep(dsys, part, xo, cur, rs[(i + 1) % 2])
+
+    for i in range(args.warmup + (args.warmup % 2)):
+        step(i)
+    torch.cuda.synchronize()
+    barrier(ws)
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        time.sleep(0.3)
+        launches0 = _lib.launch_count()
+        barrier(ws)
+        torch.cuda.synchronize()
+        start.record(stream)
+        for i in range(args.steps):
+            step(i)
+        stop.record(stream)
+        stop.synchronize()
+        launches = _lib.launch_count() - launches0
+        barrier(ws)
+    t_step = max_over_ranks(start.elapsed_time(stop) / args.steps / 1e3, ws, device)
+    value = n / t_step
+    # end to end: each rank's strip from pinned host memory and back
+    xh = xo.cpu().pin_memory()
+    rh = rs[0].cpu().pin_memory()
+
+    def e2e_step():
+        xo.copy_(xh, non_blocking=True)
+        rs[0].copy_(rh, non_blocking=True)
+        step(0)
+        xh.copy_(xo, non_blocking=True)
+        rh.copy_(rs[1], non_blocking=True)
+    t_e2e = max_over_ranks(time_events(e2e_step, max(1, args.steps), stream),
+                           ws, device)
+    if rank == 0:
+        achieved = BYTES["ne_gs"] * n / t_step / 1e9
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_step * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded U[-1,1] iterate and rhs)",
+            "config": {"workload": f"poisson_control_L{args.level}_ne_gs_sweep",
+                       "unknowns": n, "alpha": args.alpha,
+                       "gs_mode": "multicolour",
+                       "step": "ghost exchange (29 rows/side, NCCL P2P) + "
+                               "one multicolour strip sweep per rank",
+                       "l2": "x+r larger than L2 at N<=2; strips of L12 at "
+                             "N>=4 may be partly L2-resident",
+                       "parallelism": f"row strips x{ws}"},
+            "roofline": {"bound": "hbm", "achieved": achieved / ws, "peak": hbm,
+                         "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": achieved / ws / hbm, "traffic": None,
+                         "bytes_per_dof": BYTES["ne_gs"], "per": "GPU"},
+            "e2e": {"value": n / t_e2e, "unit": UNIT,
+                    "h2d_bytes_per_step": 8 * (xo.numel() + rs[0].numel()),
+                    "d2h_bytes_per_step": 8 * (xo.numel() + rs[0].numel())},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }), flush=True)
+    barrier(ws)
+
+
 def run_gpu_arm(args, ws, rank, local):
     import torch
 
@@ -410,6 +503,10 @@ def main():
     ap.add_argument("--alpha", type=float, default=1e-6)
     ap.add_argument("--mode", default="multicolour",
                     choices=["wavefront", "reference", "multicolour"])
+    ap.add_argument("--partition", default="replicas",
+                    choices=["replicas", "strips"],
+                    help="N>1: independent replicas (weak) or one L12 system "
+                         "in row strips with ghost exchange (strong)")
     ap.add_argument("--quick", action="store_true",
                     help="headline only (no kernel table / solves)")
     ap.add_argument("--no-solve-l12", action="store_true",
@@ -427,6 +524,8 @@ def main():
     ws, rank, local = dist_setup()
     if args.impl == "reference":
         run_reference_arm(args, ws, rank)
+    elif args.partition == "strips":
+        run_strip_arm(args, ws, rank, local)
     else:
         run_gpu_arm(args, ws, rank, local)
     if ws > 1:

@@ -124,6 +124,21 @@ int ocmg_ne_gs_sweep_into(const ocmg_level *lv, int mode, int forward, double *x
                           double *r_in, double *r_out, void *stream,
                           int64_t *ops);
 
+/* One multicolour NE-GS sweep of the rows [y_begin, y_end) of a structured
+ * P1 level (a rank's strip).  r_in / r_out hold the rows
+ * [slab_begin, slab_end) of both fields (field stride
+ * (slab_end - slab_begin) * n1), including the ghost rows: slab_begin <=
+ * max(0, y_begin - 29), slab_end >= min(n1, y_end + 29); the ghosts of r_in
+ * must be current (the caller's halo exchange).  x holds the strip's own rows
+ * (field stride (y_end - y_begin) * n1) and is updated in place; r_out
+ * receives the strip's own rows.  Strips tile the domain: the union of all
+ * ranks' sweeps is bit-identical to ocmg_ne_gs_sweep(mode=MULTICOLOUR).
+ * B200 addition (the reference is single-process). */
+int ocmg_ne_gs_sweep_strip(const ocmg_level *lv, int forward, int y_begin,
+                           int y_end, int slab_begin, int slab_end, double *x,
+                           const double *r_in, double *r_out, void *stream,
+                           int64_t *ops);
+
 /* Constant-mode removal of the pressure fields (pressure_mean_projection,
  * assembly.py:381-388); no-op for Poisson. */
 int ocmg_mean_project(const ocmg_level *lv, double *x, void *stream);

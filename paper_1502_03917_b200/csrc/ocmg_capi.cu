@@ -309,6 +309,9 @@ bool p1_mc_sweep(const ocmg_level *lv, bool forward, double *x, double *r,
     P.base = lv->mc.base;
     P.rem = lv->mc.rem;
     P.forward = forward ? 1 : 0;
+    P.y_begin = 0;
+    P.y_end = lv->n1;
+    P.fs_in = P.fs_out = P.fs_x = (int64_t)lv->n1 * lv->n1;
     std::copy(lv->mc_ci, lv->mc_ci + 58, &P.ci[0][0]);
     P.C = lv->mc_coef.p;
     P.rin = r;
@@ -775,6 +778,46 @@ int ocmg_ne_gs_sweep_into(const ocmg_level *lv, int mode, int forward, double *x
                                       cudaMemcpyDeviceToDevice, s));
         }
         if (ops) *ops = 2 * lv->nnz;
+    });
+}
+
+int ocmg_ne_gs_sweep_strip(const ocmg_level *lv, int forward, int y_begin,
+                           int y_end, int slab_begin, int slab_end, double *x,
+                           const double *r_in, double *r_out, void *stream,
+                           int64_t *ops) {
+    return guarded([&] {
+        OCMG_REQUIRE(lv && x && r_in && r_out, "null argument");
+        OCMG_REQUIRE(lv->kind == kP1, "strip sweeps need a structured P1 level");
+        const int n1 = lv->n1;
+        OCMG_REQUIRE(0 <= y_begin && y_begin < y_end && y_end <= n1,
+                     "strip rows out of range");
+        OCMG_REQUIRE(slab_begin <= std::max(0, y_begin - 29) &&
+                         slab_end >= std::min(n1, y_end + 29) && slab_begin >= 0 &&
+                         slab_end <= n1,
+                     "slab must hold 29 ghost rows on each side of the strip");
+        OCMG_REQUIRE(r_in != r_out, "r_in and r_out must differ");
+        int dev = 0, sms = 148;
+        OCMG_CUDA(cudaGetDevice(&dev));
+        OCMG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const McsPlan pl = mcs_plan(n1, sms, y_end - y_begin);
+        McsParams P{};
+        P.n1 = n1;
+        P.nstrips = pl.nstrips;
+        P.base = pl.base;
+        P.rem = pl.rem;
+        P.forward = forward ? 1 : 0;
+        P.y_begin = y_begin;
+        P.y_end = y_end;
+        P.fs_in = P.fs_out = (int64_t)(slab_end - slab_begin) * n1;
+        P.fs_x = (int64_t)(y_end - y_begin) * n1;
+        std::copy(lv->mc_ci, lv->mc_ci + 58, &P.ci[0][0]);
+        P.C = lv->mc_coef.p;
+        P.rin = r_in - (int64_t)slab_begin * n1;
+        P.rout = r_out - (int64_t)slab_begin * n1;
+        P.x = x - (int64_t)y_begin * n1;
+        OCMG_LAUNCH(k_p1_mc_sweep, pl.grid, mcs::NT, mcs::SMEM, as_stream(stream), P);
+        OCMG_LAUNCH_CHECK();
+        if (ops) *ops = 2 * lv->nnz * (int64_t)(y_end - y_begin) / n1;
     });
 }
 

@@ -78,8 +78,13 @@ __device__ __forceinline__ double node_update(double2 *const (&adr)[7],
 
 struct McsParams {
     int n1, nstrips, base, rem, forward;
+    int y_begin, y_end;        // rows this launch owns (a rank's strip; 0, n1)
+    int64_t fs_in, fs_out, fs_x;  // field strides of rin / rout / x
     double ci[2][29];  // interior class (3,3): W row, A row, 1/n_diag per field
     const double *C;   // [49][2][29]: W row, A row, 1/n_diag per (class, field)
+    // addressed by global vertex index y*n1+x (+ field * fs_*): rin must hold
+    // rows [y_begin-29, y_end+29) of the domain, rout and x rows
+    // [y_begin, y_end); a rank passes base pointers shifted by its slab start
     const double *rin;
     double *rout, *x;
 };
@@ -90,13 +95,14 @@ __global__ void __launch_bounds__(mcs::NT, 1)
     extern __shared__ double2 ring[];  // [RING][STRIDE] (state, adjoint)
     const int tid = threadIdx.x, lane = tid & 31, q = tid >> 5;
     const int n1 = P.n1;
-    const int64_t N = (int64_t)n1 * n1;
+    const int64_t NI = P.fs_in;
     const int strip = blockIdx.x % P.nstrips, seg = blockIdx.x / P.nstrips;
     const int nseg = P.base + (strip < P.rem ? 1 : 0);
     if (seg >= nseg) return;
-    const int seg_h = (n1 + nseg - 1) / nseg;
+    const int rows = P.y_end - P.y_begin;
+    const int seg_h = (rows + nseg - 1) / nseg;
     const int X0 = strip * W, X1 = min(n1, X0 + W);
-    const int Y0 = seg * seg_h, Y1 = min(n1, Y0 + seg_h);
+    const int Y0 = P.y_begin + seg * seg_h, Y1 = min(P.y_end, Y0 + seg_h);
     if (Y0 >= Y1) return;
     const int xl = max(0, X0 - H), xr = min(n1, X1 + H);
     const int Ylo = max(0, Y0 - H), Yhi = min(n1, Y1 + H);
@@ -112,10 +118,10 @@ __global__ void __launch_bounds__(mcs::NT, 1)
     if (tid < 2 * STRIDE)
         for (int y = Ylo - 1; y <= Ylo + 1; ++y)
             ldst[2 * STRIDE * slot0(y)] =
-                lact && y >= 0 && y <= rmax ? __ldg(P.rin + lf * N + (int64_t)y * n1 + lx)
+                lact && y >= 0 && y <= rmax ? __ldg(P.rin + lf * NI + (int64_t)y * n1 + lx)
                                             : 0.0;
     int lrow = Ylo + 2;  // next row to fetch
-    const double *lsrc = P.rin + lf * N + (int64_t)lrow * n1 + lx;
+    const double *lsrc = P.rin + lf * NI + (int64_t)lrow * n1 + lx;
     double pf[PF];       // rows s+2 .. s+1+PF in flight
 #pragma unroll
     for (int i = 0; i < PF; ++i) {
@@ -142,7 +148,7 @@ __global__ void __launch_bounds__(mcs::NT, 1)
     int o = (cm - xl - 2 * y) % 7;
     o += o < 0 ? 7 : 0;
     int sy = slot0(y);
-    double *xrow = P.x + field * N + (int64_t)y * n1 + xl + 7 * lane;
+    double *xrow = P.x + field * P.fs_x + (int64_t)y * n1 + xl + 7 * lane;
     const int xbase = xl + 7 * lane;
     auto owned = [&](int yy, int xx) {
         return yy >= Y0 && yy < Y1 && xx >= X0 && xx < X1;
@@ -164,7 +170,7 @@ __global__ void __launch_bounds__(mcs::NT, 1)
     const int sf = tid / W, sx = X0 + (tid - sf * W);
     const bool sact = tid < 2 * W && sx < X1;
     const double *ssrc = reinterpret_cast<const double *>(ring) + 2 * (sx - xl + 1) + sf;
-    double *sdst = P.rout + sf * N + (int64_t)Y0 * n1 + sx;
+    double *sdst = P.rout + sf * P.fs_out + (int64_t)Y0 * n1 + sx;
     const int s_st0 = Y0 - Ylo + 41, s_st1 = Y1 - Ylo + 41;
 
     const int nsteps = (Yhi - Ylo) + 41;
@@ -218,11 +224,12 @@ struct McsPlan {
     int nstrips = 0, base = 0, rem = 0, grid = 0;
 };
 
-inline McsPlan mcs_plan(int n1, int sm_count) {
+inline McsPlan mcs_plan(int n1, int sm_count, int rows = -1) {
     McsPlan p;
+    if (rows < 0) rows = n1;
     p.nstrips = (n1 + mcs::W - 1) / mcs::W;
     // segments much shorter than the pipeline fill (2H + 41 rows) waste steps
-    const int max_seg = std::max(1, n1 / 32);
+    const int max_seg = std::max(1, rows / 32);
     const int total = std::max(p.nstrips, std::min(sm_count, p.nstrips * max_seg));
     p.base = total / p.nstrips;
     p.rem = total % p.nstrips;
