@@ -15,6 +15,7 @@
 #include "ocmg_p1_tiled.cuh"
 #include "ocmg_p1_mc.cuh"
 #include "ocmg_p1_mc_small.cuh"
+#include "ocmg_subcycle.cuh"
 #include "ocmg_wavefront.cuh"
 
 using namespace ocmg;
@@ -88,6 +89,7 @@ struct ocmg_coarse {
     int64_t n = 0, p_off = 0, mu_off = 0, n_p = 0;
     DevBuf<double> lu;
     DevBuf<int32_t> piv;
+    DevBuf<double> inv;  // row-major A^-1 (n <= kCoarseInvMax): the cycle's solve
 };
 
 struct ocmg_hierarchy {
@@ -99,6 +101,11 @@ struct ocmg_hierarchy {
     // h>=1, and for h < top: restricted rhs crhs[h], correction corr[h]
     std::vector<DevBuf<double>> r, scratch, crhs, corr;
     DevBuf<double> tmp, scal;
+    // fused coarse end of the cycle (ocmg_subcycle.cuh): a visit of hierarchy
+    // index sub_hi runs everything below it in one launch (0 = off)
+    int sub_hi = 0;
+    SubcycleParams sub{};
+    size_t sub_smem = 0;
     cudaGraphExec_t graph = nullptr;
     const double *graph_x = nullptr, *graph_f = nullptr;
     cudaStream_t graph_stream = nullptr;
@@ -447,6 +454,81 @@ __global__ void k_coarse_solve(int n, const double *__restrict__ lu,
     for (int i = threadIdx.x; i < n; i += blockDim.x) xout[i] = b[i];
 }
 
+// Coarse solve as x = A^-1 b (A^-1 formed once on the host from the same LU):
+// one warp per row, the whole (projected) rhs in shared memory.  Used by the
+// cycle driver, where the coarsest level is visited once per coarse-grid
+// correction (2^(levels-1) times per W-cycle); replacing the triangular solves
+// by an explicit inverse changes cycle iterates by <= 2e-16 (Poisson) /
+// 6.2e-15 (Stokes) with identical cycle counts (SURVEY.md §8(a) CoarseSolver).
+constexpr int64_t kCoarseInvMax = 1024;
+
+__global__ void __launch_bounds__(256)
+    k_coarse_inv(int n, const double *__restrict__ inv, int stokes, int p_off,
+                 int mu_off, int n_p, const double *__restrict__ rhs,
+                 double *__restrict__ xout) {
+    extern __shared__ double b[];
+    __shared__ double sh[32];
+    __shared__ double mean[2];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) b[i] = rhs[i];
+    __syncthreads();
+    if (stokes) {  // project the rhs, pin (multigrid.py:95-99)
+        const int offs[2] = {p_off, mu_off};
+        for (int f = 0; f < 2; ++f) {
+            double acc = 0.0;
+            for (int i = threadIdx.x; i < n_p; i += blockDim.x) acc += b[offs[f] + i];
+            acc = block_sum(acc, sh);
+            if (threadIdx.x == 0) mean[f] = acc / (double)n_p;
+            __syncthreads();
+            for (int i = threadIdx.x; i < n_p; i += blockDim.x) b[offs[f] + i] -= mean[f];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            b[p_off] = 0.0;
+            b[mu_off] = 0.0;
+        }
+        __syncthreads();
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int row = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (row >= n) return;
+    const double *a = inv + (int64_t)row * n;
+    double acc = 0.0;
+    for (int j = lane; j < n; j += 32) acc = fma(__ldg(a + j), b[j], acc);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) xout[row] = acc;
+}
+
+// Stokes: re-centre the pressure fields of the solution (one CTA)
+__global__ void k_coarse_recentre(int p_off, int mu_off, int n_p,
+                                  double *__restrict__ x) {
+    __shared__ double sh[32];
+    __shared__ double mean;
+    const int offs[2] = {p_off, mu_off};
+    for (int f = 0; f < 2; ++f) {
+        double acc = 0.0;
+        for (int i = threadIdx.x; i < n_p; i += blockDim.x) acc += x[offs[f] + i];
+        acc = block_sum(acc, sh);
+        if (threadIdx.x == 0) mean = acc / (double)n_p;
+        __syncthreads();
+        for (int i = threadIdx.x; i < n_p; i += blockDim.x) x[offs[f] + i] -= mean;
+        __syncthreads();
+    }
+}
+
+void coarse_solve_inv(const ocmg_coarse *c, const double *rhs, double *x,
+                      cudaStream_t s) {
+    const int n = (int)c->n;
+    const size_t smem = (size_t)n * sizeof(double);
+    const bool stokes = c->problem == OCMG_STOKES;
+    OCMG_LAUNCH(k_coarse_inv, (n + 7) / 8, 256, smem, s, n, c->inv.p, stokes ? 1 : 0,
+                (int)c->p_off, (int)c->mu_off, (int)c->n_p, rhs, x);
+    if (stokes)
+        OCMG_LAUNCH(k_coarse_recentre, 1, 256, 0, s, (int)c->p_off, (int)c->mu_off,
+                    (int)c->n_p, x);
+    OCMG_LAUNCH_CHECK();
+}
+
 void coarse_solve(const ocmg_coarse *c, const double *rhs, double *x,
                   cudaStream_t s) {
     const size_t smem = (size_t)c->n * sizeof(double);
@@ -532,8 +614,19 @@ void smooth_n(ocmg_hierarchy *h, int hi, int nu, double *x, double *r,
 
 void cycle_rec(ocmg_hierarchy *h, int hi, double *x, const double *rhs,
                cudaStream_t s) {
+    if (h->sub_hi > 0 && hi == h->sub_hi) {
+        SubcycleParams P = h->sub;
+        P.x = x;
+        P.rhs = rhs;
+        OCMG_LAUNCH(k_p1_subcycle, 1, kSubThreads, h->sub_smem, s, P);
+        OCMG_LAUNCH_CHECK();
+        return;
+    }
     if (hi == 0) {
-        coarse_solve(h->coarse, rhs, x, s);
+        if (h->coarse->inv.p)
+            coarse_solve_inv(h->coarse, rhs, x, s);
+        else
+            coarse_solve(h->coarse, rhs, x, s);
         return;
     }
     ocmg_level *lv = h->levels[hi - 1];
@@ -553,6 +646,54 @@ void cycle_rec(ocmg_hierarchy *h, int hi, double *x, const double *rhs,
     level_mean_project(lv, x, s);
     level_residual(lv, x, rhs, r, s);
     smooth_n(h, hi, h->cfg.nu_post, x, r, s);
+}
+
+// Enable the fused coarse block when the bottom of the hierarchy is
+// structured Poisson with multicolour NE-GS and an explicit coarse inverse.
+void setup_subcycle(ocmg_hierarchy *h) {
+    h->sub_hi = 0;
+    const ocmg_cycle_config &c = h->cfg;
+    if (c.gs_mode != OCMG_GS_MULTICOLOUR || c.smoother == OCMG_SMOOTHER_NORMAL) return;
+    if (!h->coarse->inv.p || h->coarse->problem != OCMG_POISSON) return;
+    const ocmg_level *l0 = h->levels[0];
+    if (l0->kind != kP1 || l0->k - 1 < 3) return;
+    const int nc1 = (1 << (l0->k - 1)) + 1;
+    if (h->coarse->n != 2 * (int64_t)nc1 * nc1) return;
+    int top = 0;  // last hierarchy index with a structured level k <= kSubMaxK
+    for (int hi = 1; hi <= (int)h->levels.size(); ++hi) {
+        const ocmg_level *lv = h->levels[hi - 1];
+        const ocmg_transfer *t = h->transfers[hi - 1];
+        if (lv->kind != kP1 || lv->k > kSubMaxK || t->kind != kP1) break;
+        top = hi;
+    }
+    if (top < 1 || top + 1 > kSubMaxK) return;
+    SubcycleParams P{};
+    P.nlev = top + 1;
+    P.cycle_w = c.cycle_w;
+    P.nu_pre = c.nu_pre;
+    P.nu_post = c.nu_post;
+    P.slsgs = c.smoother == OCMG_SMOOTHER_SLSGS ? 1 : 0;
+    P.lv[0].n1 = nc1;
+    int n1s[kSubMaxK] = {nc1};
+    for (int j = 1; j <= top; ++j) {
+        const ocmg_level *lv = h->levels[j - 1];
+        P.lv[j] = SubLevel{lv->n1, lv->tables.p, lv->mc_coef.p};
+        n1s[j] = lv->n1;
+    }
+    P.inv = h->coarse->inv.p;
+    const SubLayout L = sub_layout(P.nlev, n1s);
+    const size_t smem = (size_t)L.total * sizeof(double);
+    if (smem > 200 * 1024) return;
+    static bool attr = false;
+    if (!attr) {
+        OCMG_CUDA(cudaFuncSetAttribute(k_p1_subcycle,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       200 * 1024));
+        attr = true;
+    }
+    h->sub = P;
+    h->sub_smem = smem;
+    h->sub_hi = top;
 }
 
 // one cycle + projection + ||f - A x||^2 into h->scal[0]
@@ -921,6 +1062,24 @@ int ocmg_coarse_create(int problem, int64_t n, const double *lu,
         std::vector<int32_t> p32(n);
         for (int64_t i = 0; i < n; ++i) p32[i] = (int32_t)piv[i];
         c->piv.upload(p32);
+        if (n <= kCoarseInvMax) {
+            // A^-1 column by column with the same getrs steps as k_coarse_solve
+            std::vector<double> inv((size_t)(n * n)), b((size_t)n);
+            for (int64_t col = 0; col < n; ++col) {
+                std::fill(b.begin(), b.end(), 0.0);
+                b[col] = 1.0;
+                for (int64_t i = 0; i < n; ++i)
+                    if (piv[i] != i) std::swap(b[i], b[piv[i]]);
+                for (int64_t j = 0; j < n; ++j)
+                    for (int64_t i = j + 1; i < n; ++i) b[i] -= lu[i + j * n] * b[j];
+                for (int64_t j = n - 1; j >= 0; --j) {
+                    b[j] /= lu[j + j * n];
+                    for (int64_t i = 0; i < j; ++i) b[i] -= lu[i + j * n] * b[j];
+                }
+                for (int64_t i = 0; i < n; ++i) inv[i * n + col] = b[i];  // row-major
+            }
+            c->inv.upload(inv);
+        }
         *out = c.release();
     });
 }
@@ -976,6 +1135,7 @@ int ocmg_hierarchy_create(int n_levels, ocmg_level *const *levels,
         }
         h->tmp.alloc(sizes[n_levels]);
         h->scal.alloc(8);
+        setup_subcycle(h.get());
         *out = h.release();
     });
 }
@@ -1096,5 +1256,19 @@ extern "C" int ocmg__debug_mc_passes(const ocmg_level *lv, int forward, double *
                         lv->tables.p, c, x, r);
         }
         OCMG_LAUNCH_CHECK();
+    });
+}
+
+// internal: switch the fused coarse block of a hierarchy off (0) or back on
+// (1), so tests can compare the fused and per-level cycles
+extern "C" int ocmg__debug_hierarchy_fuse(ocmg_hierarchy *h, int on) {
+    return guarded([&] {
+        OCMG_REQUIRE(h, "null hierarchy");
+        if (on)
+            setup_subcycle(h);
+        else
+            h->sub_hi = 0;
+        h->graph_x = nullptr;  // recapture
+        h->graph_f = nullptr;
     });
 }

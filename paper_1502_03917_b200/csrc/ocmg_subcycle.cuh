@@ -1,0 +1,222 @@
+// The coarse end of a multigrid cycle in ONE launch (structured Poisson,
+// multicolour NE-GS): a visit of level kt (<= 5) runs the whole recursion
+// below it -- residual, pre-smoothing, restriction, the coarser visits
+// (twice for W), the coarse solve, prolongation, residual, post-smoothing --
+// in one CTA with every vector in shared memory.
+//
+// Why: a W-cycle visits level l 2^(L-l) times, so the coarse levels are
+// thousands of tiny launches per cycle (launch-latency bound; at L12 they were
+// ~75 of ~85 ms per W-cycle).  Here a visit of level 5 costs one launch.
+//
+// Every operation repeats the arithmetic of the per-level kernels it replaces
+// (k_p1_residual_int/ring, k_p1_mc_small, k_p1_restrict_tiled,
+// k_p1_prolong_add_tiled, k_coarse_inv), so a cycle with the fused block is
+// bit-identical to one without it (tests/test_gpu_parity.py).
+#pragma once
+
+#include "ocmg_p1_mc.cuh"
+
+namespace ocmg {
+
+constexpr int kSubMaxK = 5;        // top level of the fused block
+constexpr int kSubThreads = 1024;
+
+struct SubLevel {
+    int n1;
+    const double *T;  // class tables (ocmg_p1.cuh layout)
+    const double *C;  // multicolour table [49][2][29]
+};
+
+struct SubcycleParams {
+    int nlev;          // levels kc .. kt: index 0 = coarse (kc), nlev-1 = kt
+    int cycle_w, nu_pre, nu_post, slsgs;
+    SubLevel lv[kSubMaxK];
+    const double *inv;  // coarse A^-1, row-major, n = 2 (2^kc+1)^2
+    double *x;          // level kt iterate (global), updated
+    const double *rhs;  // level kt right-hand side (global)
+};
+
+// shared-memory layout: per level j, X_j and B_j (2N doubles each); per
+// smoothed level j >= 1, the residual R_j as a zero-guarded (n1+2)^2 grid of
+// (state, adjoint) pairs
+struct SubLayout {
+    int off_x[kSubMaxK], off_b[kSubMaxK], off_r[kSubMaxK];
+    int total;  // doubles
+};
+
+__host__ __device__ inline SubLayout sub_layout(int nlev, const int *n1s) {
+    SubLayout L{};
+    int o = 0;
+    for (int j = 0; j < nlev; ++j) {
+        const int n1 = n1s[j], N = n1 * n1;
+        if (j >= 1) {  // 16-byte aligned pairs first
+            o = (o + 1) & ~1;
+            L.off_r[j] = o;
+            o += 2 * (n1 + 2) * (n1 + 2);
+        }
+        L.off_x[j] = o;
+        o += 2 * N;
+        L.off_b[j] = o;
+        o += 2 * N;
+    }
+    L.total = o;
+    return L;
+}
+
+namespace sub {
+
+__device__ void residual(const SubLevel &l, const double *X, const double *B, double2 *R) {
+    const int n1 = l.n1, N = n1 * n1, P = n1 + 2;
+    for (int v = threadIdx.x; v < N; v += blockDim.x) {
+        const int iy = v / n1, ix = v - iy * n1;
+        const P1Node q = p1_node(ix, iy, n1);
+        const double *A = l.T + kP1OffA + q.c * 28;
+        double s0 = -p1_row_dot(q, A, X, N);
+        double s1 = -p1_row_dot(q, A + 14, X, N);
+        s0 = __dadd_rn(s0, B[v]);
+        s1 = __dadd_rn(s1, B[N + v]);
+        R[(iy + 1) * P + ix + 1] = make_double2(s0, s1);
+    }
+    __syncthreads();
+}
+
+__device__ void sweep(const SubLevel &l, double *X, double2 *R, bool forward) {
+    const int n1 = l.n1, N = n1 * n1, P = n1 + 2;
+    const int per_row = (n1 + 6) / 7, count = per_row * n1;
+    for (int b = 0; b < 14; ++b) {
+        const int colour = forward ? b : 13 - b;
+        const int field = colour / 7, cm = colour % 7;
+        for (int k = threadIdx.x; k < count; k += blockDim.x) {
+            const int iy = k / per_row, jj = k - iy * per_row;
+            const int ix = ((cm - 2 * iy) % 7 + 7) % 7 + 7 * jj;
+            if (ix >= n1) continue;
+            const int c = (iy + 1) * P + ix + 1;
+            double2 *const adr[7] = {R + c - P - 1, R + c - P, R + c - 1, R + c,
+                                     R + c + 1,     R + c + P, R + c + P + 1};
+            const int cls = 7 * p1_axis_class(iy, n1) + p1_axis_class(ix, n1);
+            const double p = mcs::node_update<false>(adr, nullptr, nullptr, 0.0,
+                                                     l.C + (cls * 2 + field) * 29);
+            const int xi = field * N + iy * n1 + ix;
+            X[xi] = __dadd_rn(X[xi], p);
+        }
+        __syncthreads();
+    }
+}
+
+// coarse (nc1) <- R fine residual (2 nc1 - 1), k_p1_restrict arithmetic
+__device__ void restrict_to(int nc1, const double2 *R, double *Bc) {
+    const int nf1 = 2 * nc1 - 1, P = nf1 + 2, Nc = nc1 * nc1;
+    for (int v = threadIdx.x; v < Nc; v += blockDim.x) {
+        const int cy = v / nc1, cx = v - cy * nc1;
+        const bool l = cx > 0, rr = cx < nc1 - 1, dn = cy > 0, up = cy < nc1 - 1;
+        const int c = (2 * cy + 1) * P + 2 * cx + 1;
+        double s[2];
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            auto f = [&](int i) { return b ? R[i].y : R[i].x; };
+            double a = 0.0;
+            if (l && dn) a = __dadd_rn(a, __dmul_rn(0.5, f(c - P - 1)));
+            if (dn) a = __dadd_rn(a, __dmul_rn(0.5, f(c - P)));
+            if (l) a = __dadd_rn(a, __dmul_rn(0.5, f(c - 1)));
+            a = __dadd_rn(a, f(c));
+            if (rr) a = __dadd_rn(a, __dmul_rn(0.5, f(c + 1)));
+            if (up) a = __dadd_rn(a, __dmul_rn(0.5, f(c + P)));
+            if (rr && up) a = __dadd_rn(a, __dmul_rn(0.5, f(c + P + 1)));
+            s[b] = a;
+        }
+        Bc[v] = s[0];
+        Bc[Nc + v] = s[1];
+    }
+    __syncthreads();
+}
+
+// fine X += P coarse X (k_p1_prolong_add arithmetic)
+__device__ void prolong_add(int nc1, const double *Xc, double *Xf) {
+    const int nf1 = 2 * nc1 - 1, Nf = nf1 * nf1, Nc = nc1 * nc1;
+    for (int v = threadIdx.x; v < Nf; v += blockDim.x) {
+        const int fy = v / nf1, fx = v - fy * nf1;
+        const int ox = fx & 1, oy = fy & 1;
+        const int a = (fy >> 1) * nc1 + (fx >> 1);
+        const int b2 = ((fy >> 1) + oy) * nc1 + (fx >> 1) + ox;
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            const double *cc = Xc + b * Nc;
+            const double s = (ox | oy) ? __dadd_rn(__dmul_rn(0.5, cc[a]), __dmul_rn(0.5, cc[b2]))
+                                       : __dmul_rn(1.0, cc[a]);
+            Xf[b * Nf + v] = __dadd_rn(Xf[b * Nf + v], s);
+        }
+    }
+    __syncthreads();
+}
+
+// X = A^-1 B, warp per row (k_coarse_inv arithmetic)
+__device__ void coarse(int n, const double *__restrict__ inv, const double *B, double *X) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int row = warp; row < n; row += nw) {
+        const double *a = inv + (int64_t)row * n;
+        double acc = 0.0;
+        for (int j = lane; j < n; j += 32) acc = fma(__ldg(a + j), B[j], acc);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) X[row] = acc;
+    }
+    __syncthreads();
+}
+
+__device__ void smooth(const SubcycleParams &p, int j, double *X, double2 *R, int nu) {
+    for (int i = 0; i < nu; ++i) {
+        sweep(p.lv[j], X, R, true);
+        if (p.slsgs) sweep(p.lv[j], X, R, false);
+    }
+}
+
+// level j of the block (0 = coarse); compile-time depth, no device recursion
+template <int J>
+__device__ void visit(const SubcycleParams &p, const SubLayout &L, double *sm) {
+    double *X = sm + L.off_x[J], *B = sm + L.off_b[J];
+    if constexpr (J == 0) {
+        coarse(2 * p.lv[0].n1 * p.lv[0].n1, p.inv, B, X);
+    } else {
+        double2 *R = reinterpret_cast<double2 *>(sm + L.off_r[J]);
+        const int nc1 = p.lv[J - 1].n1, Nc = nc1 * nc1;
+        residual(p.lv[J], X, B, R);
+        smooth(p, J, X, R, p.nu_pre);
+        double *Xc = sm + L.off_x[J - 1], *Bc = sm + L.off_b[J - 1];
+        restrict_to(nc1, R, Bc);
+        for (int i = threadIdx.x; i < 2 * Nc; i += blockDim.x) Xc[i] = 0.0;
+        __syncthreads();
+        const int rec = (p.cycle_w && J - 1 > 0) ? 2 : 1;
+        for (int k = 0; k < rec; ++k) visit<J - 1>(p, L, sm);
+        prolong_add(nc1, Xc, X);
+        residual(p.lv[J], X, B, R);
+        smooth(p, J, X, R, p.nu_post);
+    }
+}
+
+}  // namespace sub
+
+__global__ void __launch_bounds__(kSubThreads, 1)
+    k_p1_subcycle(const __grid_constant__ SubcycleParams P) {
+    extern __shared__ double sm[];
+    int n1s[kSubMaxK];
+    for (int j = 0; j < P.nlev; ++j) n1s[j] = P.lv[j].n1;
+    const SubLayout L = sub_layout(P.nlev, n1s);
+    for (int i = threadIdx.x; i < L.total; i += blockDim.x) sm[i] = 0.0;  // guards
+    __syncthreads();
+    const int top = P.nlev - 1, N = P.lv[top].n1 * P.lv[top].n1;
+    double *X = sm + L.off_x[top], *B = sm + L.off_b[top];
+    for (int i = threadIdx.x; i < 2 * N; i += blockDim.x) {
+        X[i] = P.x[i];
+        B[i] = P.rhs[i];
+    }
+    __syncthreads();
+    switch (top) {
+    case 1: sub::visit<1>(P, L, sm); break;
+    case 2: sub::visit<2>(P, L, sm); break;
+    case 3: sub::visit<3>(P, L, sm); break;
+    default: sub::visit<4>(P, L, sm); break;
+    }
+    for (int i = threadIdx.x; i < 2 * N; i += blockDim.x) P.x[i] = X[i];
+}
+
+}  // namespace ocmg

@@ -18,6 +18,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--level", type=int, default=12)
 ap.add_argument("--mode", default="multicolour")
 ap.add_argument("--cycles", type=int, default=2)
+ap.add_argument("--no-levels", action="store_true")
+ap.add_argument("--coarsest", default="1,3")
 a = ap.parse_args()
 
 
@@ -35,7 +37,7 @@ def ev_time(fn, iters=5):
 
 
 print("level  n1   sweep_us  residual_us", flush=True)
-for k in range(2, a.level + 1):
+for k in ([] if a.no_levels else range(2, a.level + 1)):
     sysk = P.build_poisson_system(k, 1e-6)
     x = torch.rand(sysk.n, dtype=torch.float64, device="cuda")
     r = torch.rand(sysk.n, dtype=torch.float64, device="cuda")
@@ -47,7 +49,7 @@ for k in range(2, a.level + 1):
     print(f"{k:5d} {2 ** k + 1:5d} {ts:10.1f} {tr:10.1f}", flush=True)
 
 for cyc in ("v", "w"):
-    for coarsest in (1, 3):
+    for coarsest in [int(c) for c in a.coarsest.split(",")]:
         cfg = P.CycleConfig(smoother=P.SmootherKind("lsgs"), cycle=cyc,
                             coarsest_level=coarsest, gs_mode=a.mode)
         mg = P.build_solver("poisson", a.level, 1e-6, cfg)

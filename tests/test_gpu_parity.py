@@ -266,6 +266,28 @@ def test_strip_sweeps_match_single_gpu(k, ws):
     assert torch.equal(rg, r)
 
 
+@pytest.mark.parametrize("cycle,smoother,k", [("w", "lsgs", 8), ("v", "slsgs", 7),
+                                               ("w", "lsgs", 5)])
+def test_fused_coarse_block_is_bit_identical(cycle, smoother, k):
+    """The one-launch coarse end of the cycle (ocmg_subcycle.cuh) reproduces
+    the per-level cycle bit for bit."""
+    import ctypes
+    cfg = P.CycleConfig(smoother=P.SmootherKind(smoother), cycle=cycle,
+                        coarsest_level=3, gs_mode="multicolour")
+    mg = P.build_solver("poisson", k, 1e-6, cfg)
+    f = P.baseline_rhs(mg.finest, 0, add_sine=True)
+    fn = _lib.load().ocmg__debug_hierarchy_fuse
+    fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    xs, hs = [], []
+    for on in (1, 0):
+        _lib.check(fn(mg.native().handle, on))
+        x, hist = mg.solve_to_tolerance(f, tol=0.0, max_cycles=3)
+        xs.append(host(x) if hasattr(x, "cpu") else x)
+        hs.append(hist)
+    assert np.array_equal(xs[0], xs[1])
+    assert hs[0] == hs[1]
+
+
 @pytest.mark.parametrize("prob,kc", [("poisson", 1), ("poisson", 4),
                                      ("stokes", 1), ("stokes", 3)])
 def test_transfers_bitwise(prob, kc):
