@@ -669,10 +669,11 @@ void setup_subcycle(ocmg_hierarchy *h) {
     if (top < 1 || top + 1 > kSubMaxK) return;
     SubcycleParams P{};
     P.nlev = top + 1;
-    P.cycle_w = c.cycle_w;
-    P.nu_pre = c.nu_pre;
-    P.nu_post = c.nu_post;
-    P.slsgs = c.smoother == OCMG_SMOOTHER_SLSGS ? 1 : 0;
+    std::vector<unsigned short> ops;
+    sub_ops(top, c.cycle_w, c.nu_pre, c.nu_post, c.smoother == OCMG_SMOOTHER_SLSGS, ops);
+    if ((int)ops.size() > kSubMaxOps) return;
+    P.nops = (int)ops.size();
+    std::copy(ops.begin(), ops.end(), P.ops);
     P.lv[0].n1 = nc1;
     int n1s[kSubMaxK] = {nc1};
     for (int j = 1; j <= top; ++j) {
@@ -1270,5 +1271,22 @@ extern "C" int ocmg__debug_hierarchy_fuse(ocmg_hierarchy *h, int on) {
             h->sub_hi = 0;
         h->graph_x = nullptr;  // recapture
         h->graph_f = nullptr;
+    });
+}
+
+// internal: one launch of a hierarchy's fused coarse block on (x, rhs), with
+// per-op timestamps into prof (device, nops + 1 entries); returns nops
+extern "C" int ocmg__debug_subcycle_prof(ocmg_hierarchy *h, double *x, const double *rhs,
+                                         unsigned long long *prof, int *nops) {
+    return guarded([&] {
+        OCMG_REQUIRE(h && h->sub_hi > 0, "no fused block");
+        SubcycleParams P = h->sub;
+        P.x = x;
+        P.rhs = rhs;
+        P.prof = prof;
+        *nops = P.nops;
+        OCMG_LAUNCH(k_p1_subcycle, 1, kSubThreads, h->sub_smem, nullptr, P);
+        OCMG_LAUNCH_CHECK();
+        OCMG_CUDA(cudaDeviceSynchronize());
     });
 }

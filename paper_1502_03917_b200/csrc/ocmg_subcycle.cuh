@@ -19,7 +19,7 @@
 namespace ocmg {
 
 constexpr int kSubMaxK = 5;        // top level of the fused block
-constexpr int kSubThreads = 1024;
+constexpr int kSubThreads = 256;
 
 struct SubLevel {
     int n1;
@@ -27,13 +27,22 @@ struct SubLevel {
     const double *C;  // multicolour table [49][2][29]
 };
 
+// The block's work as a flat op list (built on the host by unrolling the
+// V/W recursion), executed by one loop with each operation's code present
+// once: a template-unrolled recursion inlined every operation per level and
+// visit, and the kernel ran out of instruction cache.
+enum SubOp : int { kOpResid = 0, kOpSweepF, kOpSweepB, kOpRestrict, kOpCoarse, kOpProlong };
+constexpr int kSubMaxOps = 256;
+
 struct SubcycleParams {
     int nlev;          // levels kc .. kt: index 0 = coarse (kc), nlev-1 = kt
-    int cycle_w, nu_pre, nu_post, slsgs;
+    int nops;
+    unsigned short ops[kSubMaxOps];  // (op << 4) | level j
     SubLevel lv[kSubMaxK];
     const double *inv;  // coarse A^-1, row-major, n = 2 (2^kc+1)^2
     double *x;          // level kt iterate (global), updated
     const double *rhs;  // level kt right-hand side (global)
+    unsigned long long *prof;  // debug: %globaltimer at each op (or null)
 };
 
 // shared-memory layout: per level j, X_j and B_j (2N doubles each); per
@@ -41,6 +50,7 @@ struct SubcycleParams {
 // (state, adjoint) pairs
 struct SubLayout {
     int off_x[kSubMaxK], off_b[kSubMaxK], off_r[kSubMaxK];
+    int off_a[kSubMaxK], off_c[kSubMaxK];  // A rows [49][28], mc table [49][2][29]
     int total;  // doubles
 };
 
@@ -58,6 +68,13 @@ __host__ __device__ inline SubLayout sub_layout(int nlev, const int *n1s) {
         o += 2 * N;
         L.off_b[j] = o;
         o += 2 * N;
+        if (j >= 1) {  // the level's coefficients: shared memory, not L1 (the
+                       // coarse inverse streams through L1 every visit)
+            L.off_a[j] = o;
+            o += 49 * 28;
+            L.off_c[j] = o;
+            o += 49 * 2 * 29;
+        }
     }
     L.total = o;
     return L;
@@ -65,23 +82,55 @@ __host__ __device__ inline SubLayout sub_layout(int nlev, const int *n1s) {
 
 namespace sub {
 
-__device__ void residual(const SubLevel &l, const double *X, const double *B, double2 *R) {
-    const int n1 = l.n1, N = n1 * n1, P = n1 + 2;
+__device__ __forceinline__ void residual(int n1, const double *At, const double *X,
+                                         const double *B, double2 *R) {
+    const int N = n1 * n1, P = n1 + 2;
     for (int v = threadIdx.x; v < N; v += blockDim.x) {
         const int iy = v / n1, ix = v - iy * n1;
         const P1Node q = p1_node(ix, iy, n1);
-        const double *A = l.T + kP1OffA + q.c * 28;
-        double s0 = -p1_row_dot(q, A, X, N);
-        double s1 = -p1_row_dot(q, A + 14, X, N);
-        s0 = __dadd_rn(s0, B[v]);
-        s1 = __dadd_rn(s1, B[N + v]);
-        R[(iy + 1) * P + ix + 1] = make_double2(s0, s1);
+        const double *A = At + q.c * 28;
+        double s[2];
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {  // p1_row_dot order
+            double acc = 0.0;
+#pragma unroll
+            for (int d = 0; d < 7; ++d)
+                if (q.ex[d]) acc = __dadd_rn(acc, __dmul_rn(A[14 * b + d], X[q.nb[d]]));
+#pragma unroll
+            for (int d = 0; d < 7; ++d)
+                if (q.ex[d]) acc = __dadd_rn(acc, __dmul_rn(A[14 * b + 7 + d], X[N + q.nb[d]]));
+            s[b] = -acc;
+        }
+        R[(iy + 1) * P + ix + 1] =
+            make_double2(__dadd_rn(s[0], B[v]), __dadd_rn(s[1], B[N + v]));
     }
     __syncthreads();
 }
 
-__device__ void sweep(const SubLevel &l, double *X, double2 *R, bool forward) {
-    const int n1 = l.n1, N = n1 * n1, P = n1 + 2;
+// mcs::node_update<false> with the table in shared memory; neighbours of the
+// padded-grid cell c (row pitch P) addressed directly (no pointer array)
+__device__ __forceinline__ double node_update_sm(double2 *R, int c, int P, const double *tc) {
+    const int off[7] = {-P - 1, -P, -1, 0, 1, P, P + 1};
+    double2 v[7];
+#pragma unroll
+    for (int d = 0; d < 7; ++d) v[d] = R[c + off[d]];
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int d = 0; d < 7; ++d) {
+        s0 = __fma_rn(tc[d], v[d].x, s0);
+        s1 = __fma_rn(tc[7 + d], v[d].y, s1);
+    }
+    const double p = __dmul_rn(__dadd_rn(s0, s1), tc[28]);
+#pragma unroll
+    for (int d = 0; d < 7; ++d)
+        R[c + off[d]] = make_double2(__fma_rn(-tc[14 + d], p, v[d].x),
+                                     __fma_rn(-tc[21 + d], p, v[d].y));
+    return p;
+}
+
+__device__ __forceinline__ void sweep(int n1, const double *Ct, double *X, double2 *R,
+                                      bool forward) {
+    const int N = n1 * n1, P = n1 + 2;
     const int per_row = (n1 + 6) / 7, count = per_row * n1;
     for (int b = 0; b < 14; ++b) {
         const int colour = forward ? b : 13 - b;
@@ -91,11 +140,8 @@ __device__ void sweep(const SubLevel &l, double *X, double2 *R, bool forward) {
             const int ix = ((cm - 2 * iy) % 7 + 7) % 7 + 7 * jj;
             if (ix >= n1) continue;
             const int c = (iy + 1) * P + ix + 1;
-            double2 *const adr[7] = {R + c - P - 1, R + c - P, R + c - 1, R + c,
-                                     R + c + 1,     R + c + P, R + c + P + 1};
             const int cls = 7 * p1_axis_class(iy, n1) + p1_axis_class(ix, n1);
-            const double p = mcs::node_update<false>(adr, nullptr, nullptr, 0.0,
-                                                     l.C + (cls * 2 + field) * 29);
+            const double p = node_update_sm(R, c, P, Ct + (cls * 2 + field) * 29);
             const int xi = field * N + iy * n1 + ix;
             X[xi] = __dadd_rn(X[xi], p);
         }
@@ -104,7 +150,7 @@ __device__ void sweep(const SubLevel &l, double *X, double2 *R, bool forward) {
 }
 
 // coarse (nc1) <- R fine residual (2 nc1 - 1), k_p1_restrict arithmetic
-__device__ void restrict_to(int nc1, const double2 *R, double *Bc) {
+__device__ __forceinline__ void restrict_to(int nc1, const double2 *R, double *Bc) {
     const int nf1 = 2 * nc1 - 1, P = nf1 + 2, Nc = nc1 * nc1;
     for (int v = threadIdx.x; v < Nc; v += blockDim.x) {
         const int cy = v / nc1, cx = v - cy * nc1;
@@ -131,7 +177,7 @@ __device__ void restrict_to(int nc1, const double2 *R, double *Bc) {
 }
 
 // fine X += P coarse X (k_p1_prolong_add arithmetic)
-__device__ void prolong_add(int nc1, const double *Xc, double *Xf) {
+__device__ __forceinline__ void prolong_add(int nc1, const double *Xc, double *Xf) {
     const int nf1 = 2 * nc1 - 1, Nf = nf1 * nf1, Nc = nc1 * nc1;
     for (int v = threadIdx.x; v < Nf; v += blockDim.x) {
         const int fy = v / nf1, fx = v - fy * nf1;
@@ -150,47 +196,17 @@ __device__ void prolong_add(int nc1, const double *Xc, double *Xf) {
 }
 
 // X = A^-1 B, warp per row (k_coarse_inv arithmetic)
-__device__ void coarse(int n, const double *__restrict__ inv, const double *B, double *X) {
+__device__ __forceinline__ void coarse(int n, const double *__restrict__ inv, const double *B, double *X) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     for (int row = warp; row < n; row += nw) {
         const double *a = inv + (int64_t)row * n;
         double acc = 0.0;
-        for (int j = lane; j < n; j += 32) acc = fma(__ldg(a + j), B[j], acc);
+        for (int j = lane; j < n; j += 32) acc = fma(__ldcs(a + j), B[j], acc);
 #pragma unroll
         for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (lane == 0) X[row] = acc;
     }
     __syncthreads();
-}
-
-__device__ void smooth(const SubcycleParams &p, int j, double *X, double2 *R, int nu) {
-    for (int i = 0; i < nu; ++i) {
-        sweep(p.lv[j], X, R, true);
-        if (p.slsgs) sweep(p.lv[j], X, R, false);
-    }
-}
-
-// level j of the block (0 = coarse); compile-time depth, no device recursion
-template <int J>
-__device__ void visit(const SubcycleParams &p, const SubLayout &L, double *sm) {
-    double *X = sm + L.off_x[J], *B = sm + L.off_b[J];
-    if constexpr (J == 0) {
-        coarse(2 * p.lv[0].n1 * p.lv[0].n1, p.inv, B, X);
-    } else {
-        double2 *R = reinterpret_cast<double2 *>(sm + L.off_r[J]);
-        const int nc1 = p.lv[J - 1].n1, Nc = nc1 * nc1;
-        residual(p.lv[J], X, B, R);
-        smooth(p, J, X, R, p.nu_pre);
-        double *Xc = sm + L.off_x[J - 1], *Bc = sm + L.off_b[J - 1];
-        restrict_to(nc1, R, Bc);
-        for (int i = threadIdx.x; i < 2 * Nc; i += blockDim.x) Xc[i] = 0.0;
-        __syncthreads();
-        const int rec = (p.cycle_w && J - 1 > 0) ? 2 : 1;
-        for (int k = 0; k < rec; ++k) visit<J - 1>(p, L, sm);
-        prolong_add(nc1, Xc, X);
-        residual(p.lv[J], X, B, R);
-        smooth(p, J, X, R, p.nu_post);
-    }
 }
 
 }  // namespace sub
@@ -203,6 +219,12 @@ __global__ void __launch_bounds__(kSubThreads, 1)
     const SubLayout L = sub_layout(P.nlev, n1s);
     for (int i = threadIdx.x; i < L.total; i += blockDim.x) sm[i] = 0.0;  // guards
     __syncthreads();
+    for (int j = 1; j < P.nlev; ++j) {
+        for (int i = threadIdx.x; i < 49 * 28; i += blockDim.x)
+            sm[L.off_a[j] + i] = P.lv[j].T[kP1OffA + i];
+        for (int i = threadIdx.x; i < 49 * 58; i += blockDim.x)
+            sm[L.off_c[j] + i] = P.lv[j].C[i];
+    }
     const int top = P.nlev - 1, N = P.lv[top].n1 * P.lv[top].n1;
     double *X = sm + L.off_x[top], *B = sm + L.off_b[top];
     for (int i = threadIdx.x; i < 2 * N; i += blockDim.x) {
@@ -210,13 +232,55 @@ __global__ void __launch_bounds__(kSubThreads, 1)
         B[i] = P.rhs[i];
     }
     __syncthreads();
-    switch (top) {
-    case 1: sub::visit<1>(P, L, sm); break;
-    case 2: sub::visit<2>(P, L, sm); break;
-    case 3: sub::visit<3>(P, L, sm); break;
-    default: sub::visit<4>(P, L, sm); break;
+    for (int t = 0; t < P.nops; ++t) {
+        const int op = P.ops[t] >> 4, j = P.ops[t] & 15;
+        if (P.prof && threadIdx.x == 0) {
+            unsigned long long g;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+            P.prof[t] = g;
+        }
+        double *Xj = sm + L.off_x[j], *Bj = sm + L.off_b[j];
+        double2 *Rj = reinterpret_cast<double2 *>(sm + L.off_r[j]);
+        switch (op) {
+        case kOpResid: sub::residual(P.lv[j].n1, sm + L.off_a[j], Xj, Bj, Rj); break;
+        case kOpSweepF: sub::sweep(P.lv[j].n1, sm + L.off_c[j], Xj, Rj, true); break;
+        case kOpSweepB: sub::sweep(P.lv[j].n1, sm + L.off_c[j], Xj, Rj, false); break;
+        case kOpRestrict: {  // B_{j-1} = R R_j, X_{j-1} = 0
+            const int nc1 = P.lv[j - 1].n1;
+            double *Xc = sm + L.off_x[j - 1];
+            for (int i = threadIdx.x; i < 2 * nc1 * nc1; i += blockDim.x) Xc[i] = 0.0;
+            sub::restrict_to(nc1, Rj, sm + L.off_b[j - 1]);
+            break;
+        }
+        case kOpCoarse: sub::coarse(2 * P.lv[0].n1 * P.lv[0].n1, P.inv, Bj, Xj); break;
+        default: sub::prolong_add(P.lv[j - 1].n1, sm + L.off_x[j - 1], Xj); break;
+        }
     }
     for (int i = threadIdx.x; i < 2 * N; i += blockDim.x) P.x[i] = X[i];
+}
+
+// host: the op list of one visit of level j (mirrors cycle_rec)
+inline void sub_ops(int j, int cycle_w, int nu_pre, int nu_post, bool slsgs,
+                    std::vector<unsigned short> &ops) {
+    auto push = [&](int op, int lev) { ops.push_back((unsigned short)((op << 4) | lev)); };
+    if (j == 0) {
+        push(kOpCoarse, 0);
+        return;
+    }
+    auto smooth = [&](int nu) {
+        for (int i = 0; i < nu; ++i) {
+            push(kOpSweepF, j);
+            if (slsgs) push(kOpSweepB, j);
+        }
+    };
+    push(kOpResid, j);
+    smooth(nu_pre);
+    push(kOpRestrict, j);
+    const int rec = (cycle_w && j - 1 > 0) ? 2 : 1;
+    for (int k = 0; k < rec; ++k) sub_ops(j - 1, cycle_w, nu_pre, nu_post, slsgs, ops);
+    push(kOpProlong, j);
+    push(kOpResid, j);
+    smooth(nu_post);
 }
 
 }  // namespace ocmg
