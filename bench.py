@@ -241,7 +241,7 @@ def kernel_table(dsys, coarse_sys, transfer, x, r, f, stream, iters, hbm):
     return rows
 
 
-def solve_timing(level, alpha, cycle, coarsest, mode, sine):
+def solve_timing(level, alpha, cycle, coarsest, mode, sine, problem="poisson"):
     """Time to 1e-8 relative residual (BASELINE protocol), setup excluded."""
     import torch
 
@@ -249,8 +249,9 @@ def solve_timing(level, alpha, cycle, coarsest, mode, sine):
     t_setup = time.perf_counter()
     cfg = P.CycleConfig(smoother=P.SmootherKind("lsgs"), cycle=cycle,
                         coarsest_level=coarsest, gs_mode=mode)
-    mg = P.build_solver("poisson", level, alpha, cfg)
-    f = P.baseline_rhs(mg.finest, 0, add_sine=sine)
+    mg = P.build_solver(problem, level, alpha, cfg)
+    f = P.baseline_rhs(mg.finest, 0 if problem == "poisson" else 1,
+                       add_sine=sine)
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t_setup
     mg.solve_to_tolerance(f, tol=1e-8, max_cycles=2)      # graph capture
@@ -259,7 +260,7 @@ def solve_timing(level, alpha, cycle, coarsest, mode, sine):
     _, hist = mg.solve_to_tolerance(f, tol=1e-8, max_cycles=300)
     torch.cuda.synchronize()
     t = time.perf_counter() - t0
-    return {"config": f"poisson L{level} alpha={alpha} {cycle.upper()}(2,2) "
+    return {"config": f"{problem} L{level} alpha={alpha} {cycle.upper()}(2,2) "
                       f"NE-GS[{mode}] coarsest L{coarsest}"
                       + (" y_D=U+sin*sin" if sine else ""),
             "cycles": len(hist), "final_rel_residual": hist[-1],
@@ -473,6 +474,12 @@ def run_gpu_arm(args, ws, rank, local):
             result["modes"][other] = {"dof_per_s": n / t_o, "ms": t_o * 1e3}
             result["solve"] = [solve_timing(10, 1e-4, "v", 2, m, False)
                                for m in ("multicolour", "wavefront")]
+            # Stokes control (configs 4 and 5; generic CSR kernels)
+            result["solve"] += [solve_timing(5, 1e-4, "v", 1, m, False, "stokes")
+                                for m in ("wavefront", "multicolour")]
+            if not args.no_stokes_l10:
+                result["solve"].append(
+                    solve_timing(10, 1e-2, "v", 1, "wavefront", False, "stokes"))
             if not args.no_solve_l12:
                 modes = ["multicolour"] + (["wavefront"]
                                            if args.solve_l12_wavefront else [])
@@ -509,6 +516,8 @@ def main():
                          "in row strips with ghost exchange (strong)")
     ap.add_argument("--quick", action="store_true",
                     help="headline only (no kernel table / solves)")
+    ap.add_argument("--no-stokes-l10", action="store_true",
+                    help="skip the config-5 Stokes L10 solve (~80 s incl. setup)")
     ap.add_argument("--no-solve-l12", action="store_true",
                     help="skip the config-3 W-cycle solves at L12")
     ap.add_argument("--solve-l12-wavefront", action="store_true",
