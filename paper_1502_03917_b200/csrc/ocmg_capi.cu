@@ -109,8 +109,13 @@ struct ocmg_hierarchy {
     cudaGraphExec_t graph = nullptr;
     const double *graph_x = nullptr, *graph_f = nullptr;
     cudaStream_t graph_stream = nullptr;
+    // legacy-default-stream callers: graphs run on this stream instead
+    cudaStream_t own_stream = nullptr;
+    cudaEvent_t own_event = nullptr;
     ~ocmg_hierarchy() {
         if (graph) cudaGraphExecDestroy(graph);
+        if (own_event) cudaEventDestroy(own_event);
+        if (own_stream) cudaStreamDestroy(own_stream);
     }
 };
 
@@ -1158,6 +1163,17 @@ int ocmg_solve(ocmg_hierarchy *h, double *x, const double *f, double tol,
     return guarded([&] {
         OCMG_REQUIRE(h && x && f && hist && n_done, "null argument");
         cudaStream_t s = as_stream(stream);
+        if (use_graph && s == nullptr) {
+            // the legacy default stream cannot be captured: run the solve on
+            // a private non-blocking stream ordered after the caller's work
+            if (!h->own_stream) {
+                OCMG_CUDA(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
+                OCMG_CUDA(cudaEventCreateWithFlags(&h->own_event, cudaEventDisableTiming));
+            }
+            OCMG_CUDA(cudaEventRecord(h->own_event, nullptr));
+            OCMG_CUDA(cudaStreamWaitEvent(h->own_stream, h->own_event, 0));
+            s = h->own_stream;
+        }
         ocmg_level *fine = h->levels.back();
         // ||f||^2
         sumsq(fine->n, f, nullptr, fine->partial.p, h->scal.p + 1, s);

@@ -117,9 +117,21 @@ __device__ __forceinline__ void csr_gs_row(int32_t i, const int64_t *__restrict_
         q = __dadd_rn(q, __dmul_rn(w[t], r[col[t]]));
     const double p = __ddiv_rn(q, ndiag[i]);
     x[i] = __dadd_rn(x[i], p);
-    for (int64_t t = b; t < e; ++t) {
-        const int32_t j = col[t];
-        r[j] = __dsub_rn(r[j], __dmul_rn(val[t], p));
+    // the columns of a row are distinct, so a batch of loads may precede its
+    // stores (one-at-a-time read-modify-writes serialize on L2 latency)
+    constexpr int kB = 8;
+    for (int64_t t0 = b; t0 < e; t0 += kB) {
+        double rv[kB];
+        int32_t jv[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u)
+            if (t0 + u < e) {
+                jv[u] = col[t0 + u];
+                rv[u] = r[jv[u]];
+            }
+#pragma unroll
+        for (int u = 0; u < kB; ++u)
+            if (t0 + u < e) r[jv[u]] = __dsub_rn(rv[u], __dmul_rn(val[t0 + u], p));
     }
 }
 

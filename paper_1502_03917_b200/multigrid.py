@@ -225,8 +225,14 @@ class Multigrid:
         cycle).  Returns (x, rel_history)."""
         system = self.finest
         fd, _ = as_device(f, system.n)
-        if x is None:
-            x = zeros(system.n)
+        fresh = x is None
+        if fresh:
+            # a persistent start buffer keeps the captured cycle graph valid
+            # across calls (the graph is keyed on the x and f pointers)
+            if getattr(self, "_x0", None) is None:
+                self._x0 = zeros(system.n)
+            x = self._x0
+            x.zero_()
         xd, xnp = as_device(x, system.n)
         hist = np.zeros(max_cycles)
         done = ctypes.c_int()
@@ -235,6 +241,8 @@ class Multigrid:
                   1 if use_graph else 0, _lib.hptr(hist), ctypes.byref(done),
                   _lib.stream_ptr())
         back_inplace(xd, x, xnp)
+        if fresh:
+            x = x.clone()
         return x, hist[:done.value].tolist()
 
 
