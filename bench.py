@@ -289,7 +289,7 @@ def run_strip_arm(args, ws, rank, local):
     x = torch.rand(n, dtype=torch.float64, device=device, generator=g) * 2 - 1
     f = torch.rand(n, dtype=torch.float64, device=device, generator=g) * 2 - 1
     r = dsys.residual(x, f)
-    xo = part.scatter_own(x)
+    xo = part.scatter(x)
     rs = [part.scatter(r), torch.empty((2, part.slab_rows, n1),
                                        dtype=torch.float64, device=device)]
     del x, f, r
@@ -332,6 +332,31 @@ def run_strip_arm(args, ws, rank, local):
         rh.copy_(rs[1], non_blocking=True)
     t_e2e = max_over_ranks(time_events(e2e_step, max(1, args.steps), stream),
                            ws, device)
+    # config 3 on the partition: W(2,2) multicolour cycle, coarsest L3
+    from paper_1502_03917_b200.strips import (DistComm, LoopbackComm,
+                                              StripMultigrid)
+    solve = None
+    e2e_bytes = 8 * (xo.numel() + rs[0].numel())
+    if not args.no_solve_l12:
+        del rs, xo
+        cfg = P.CycleConfig(smoother=P.SmootherKind("lsgs"), cycle="w",
+                            coarsest_level=3, gs_mode="multicolour")
+        mg = P.build_solver("poisson", args.level, args.alpha, cfg)
+        fs = P.baseline_rhs(mg.finest, 0, add_sine=True)
+        sm = StripMultigrid(mg, ws, [rank], DistComm() if ws > 1 else LoopbackComm())
+        sm.load(fs)
+        torch.cuda.synchronize()
+        barrier(ws)
+        t0 = time.perf_counter()
+        hist = sm.solve(tol=1e-8, max_cycles=300)
+        torch.cuda.synchronize()
+        t_solve = max_over_ranks(time.perf_counter() - t0, ws, device)
+        solve = {"config": f"poisson L{args.level} alpha={args.alpha} W(2,2) "
+                           "NE-GS[multicolour] coarsest L3 y_D=U+sin*sin, "
+                           f"row strips x{ws} (levels >= "
+                           f"{mg.systems[sm.first].level} partitioned)",
+                 "cycles": len(hist), "final_rel_residual": hist[-1],
+                 "seconds": t_solve}
     if rank == 0:
         achieved = BYTES["ne_gs"] * n / t_step / 1e9
         print(json.dumps({
@@ -353,10 +378,11 @@ def run_strip_arm(args, ws, rank, local):
                          "frac": achieved / ws / hbm, "traffic": None,
                          "bytes_per_dof": BYTES["ne_gs"], "per": "GPU"},
             "e2e": {"value": n / t_e2e, "unit": UNIT,
-                    "h2d_bytes_per_step": 8 * (xo.numel() + rs[0].numel()),
-                    "d2h_bytes_per_step": 8 * (xo.numel() + rs[0].numel())},
+                    "h2d_bytes_per_step": e2e_bytes,
+                    "d2h_bytes_per_step": e2e_bytes},
             "gpu_launches": launches,
             "clocks": clk.summary(),
+            "solve": [solve] if solve else [],
         }), flush=True)
     barrier(ws)
 

@@ -125,19 +125,30 @@ int ocmg_ne_gs_sweep_into(const ocmg_level *lv, int mode, int forward, double *x
                           int64_t *ops);
 
 /* One multicolour NE-GS sweep of the rows [y_begin, y_end) of a structured
- * P1 level (a rank's strip).  r_in / r_out hold the rows
- * [slab_begin, slab_end) of both fields (field stride
- * (slab_end - slab_begin) * n1), including the ghost rows: slab_begin <=
- * max(0, y_begin - 29), slab_end >= min(n1, y_end + 29); the ghosts of r_in
- * must be current (the caller's halo exchange).  x holds the strip's own rows
- * (field stride (y_end - y_begin) * n1) and is updated in place; r_out
- * receives the strip's own rows.  Strips tile the domain: the union of all
- * ranks' sweeps is bit-identical to ocmg_ne_gs_sweep(mode=MULTICOLOUR).
- * B200 addition (the reference is single-process). */
+ * P1 level (a rank's strip).  x, r_in and r_out hold the
+ * rows [slab_begin, slab_end) of both fields (field stride
+ * (slab_end - slab_begin) * n1; a full-size vector is the slab [0, n1)),
+ * with slab_begin <= max(0, y_begin - 29) and slab_end >= min(n1, y_end + 29);
+ * the ghost rows of r_in must be current (the caller's halo exchange).  x is
+ * updated in place on the strip's rows; r_out receives the strip's rows.
+ * Strips tile the domain: the union of all ranks' sweeps is bit-identical to
+ * ocmg_ne_gs_sweep(mode=MULTICOLOUR).  B200 addition (the reference is
+ * single-process). */
 int ocmg_ne_gs_sweep_strip(const ocmg_level *lv, int forward, int y_begin,
                            int y_end, int slab_begin, int slab_end, double *x,
                            const double *r_in, double *r_out, void *stream,
                            int64_t *ops);
+
+/* Row-range forms for strip partitions (full-size vectors, only the rows
+ * [begin, end) of the output computed; inputs need their ghost rows: one row
+ * of x for the residual, one fine row for the restriction, one coarse row
+ * for the prolongation).  Structured P1 levels/transfers only. */
+int ocmg_residual_rows(const ocmg_level *lv, const double *x, const double *f,
+                       double *r, int y_begin, int y_end, void *stream);
+int ocmg_restrict_rows(const ocmg_transfer *t, const double *rf, double *rc,
+                       int cy_begin, int cy_end, void *stream);
+int ocmg_prolong_add_rows(const ocmg_transfer *t, const double *c, double *xf,
+                          int fy_begin, int fy_end, void *stream);
 
 /* Constant-mode removal of the pressure fields (pressure_mean_projection,
  * assembly.py:381-388); no-op for Poisson. */

@@ -68,6 +68,9 @@ SIGNATURES = {
                                    ctypes.POINTER(_I64)]),
     "ocmg_ne_gs_sweep_strip": (_I, [_P, _I, _I, _I, _I, _I, _P, _P, _P, _P,
                                     ctypes.POINTER(_I64)]),
+    "ocmg_residual_rows": (_I, [_P, _P, _P, _P, _I, _I, _P]),
+    "ocmg_restrict_rows": (_I, [_P, _P, _P, _I, _I, _P]),
+    "ocmg_prolong_add_rows": (_I, [_P, _P, _P, _I, _I, _P]),
     "ocmg_mean_project": (_I, [_P, _P, _P]),
     "ocmg_norm2": (_I, [_P, _P, _I, _P, _P]),
     "ocmg_transfer_create_csr": (_I, [_I64, _I64, _P, _P, _P, _PP]),

@@ -233,13 +233,21 @@ dim3 p1_interior_grid(int n1) {
     return dim3((m + kTX - 1) / kTX, (m + kTY * kRPT - 1) / (kTY * kRPT));
 }
 
+// rows [ylo, yhi) of a structured level (a rank's strip); the whole level
+// by default
 void level_residual(const ocmg_level *lv, const double *x, const double *f,
-                    double *r, cudaStream_t s) {
+                    double *r, cudaStream_t s, int ylo = 0, int yhi = -1) {
     if (lv->kind == kP1) {
-        const dim3 g = p1_interior_grid(lv->n1), b(kTX, kTY);
-        OCMG_LAUNCH(k_p1_residual_int, g, b, 0, s, lv->n1, lv->cA, x, f, r);
+        if (yhi < 0) yhi = lv->n1;
+        const int rlo = std::max(kRing, ylo), rhi = std::min(lv->n1 - kRing, yhi);
+        const int m = lv->n1 - 2 * kRing;
+        if (rhi > rlo) {
+            const dim3 g((m + kTX - 1) / kTX, (rhi - rlo + kTY * kRPT - 1) / (kTY * kRPT));
+            OCMG_LAUNCH(k_p1_residual_int, g, dim3(kTX, kTY), 0, s, lv->n1, lv->cA, x, f,
+                        r, ylo, yhi);
+        }
         OCMG_LAUNCH(k_p1_residual_ring, grid_for(p1_ring_count(lv->n1, kRing), kBlk),
-                    kBlk, 0, s, lv->n1, lv->tables.p, x, f, r);
+                    kBlk, 0, s, lv->n1, lv->tables.p, x, f, r, ylo, yhi);
     } else {
         OCMG_LAUNCH(k_csr_residual, grid_for(lv->n, kBlk), kBlk, 0, s, 
             lv->n, lv->A.off.p, lv->A.col.p, lv->A.val.p, x, f, r);
@@ -547,12 +555,14 @@ void coarse_solve(const ocmg_coarse *c, const double *rhs, double *x,
 // transfers
 // ---------------------------------------------------------------------------
 void do_restrict(const ocmg_transfer *t, const double *rf, double *rc,
-                 cudaStream_t s) {
+                 cudaStream_t s, int cylo = 0, int cyhi = -1) {
     if (t->kind == kP1) {
-        const int m = t->nc1;
-        const dim3 g((m + kTX - 1) / kTX, (m + kTY * kRPT - 1) / (kTY * kRPT));
+        if (cyhi < 0) cyhi = t->nc1;
+        const int m = t->nc1, rows = cyhi - cylo;
+        if (rows <= 0) return;
+        const dim3 g((m + kTX - 1) / kTX, (rows + kTY * kRPT - 1) / (kTY * kRPT));
         OCMG_LAUNCH(k_p1_restrict_tiled, g, dim3(kTX, kTY), 0, s, t->nc1, t->n_fields,
-                    rf, rc);
+                    rf, rc, cylo, cyhi);
     } else {
         OCMG_LAUNCH(k_csr_spmv, grid_for(t->nc, kBlk), kBlk, 0, s, 
             t->nc, t->R.off.p, t->R.col.p, t->R.val.p, rf, rc);
@@ -561,13 +571,15 @@ void do_restrict(const ocmg_transfer *t, const double *rf, double *rc,
 }
 
 void do_prolong_add(const ocmg_transfer *t, const double *c, double *xf,
-                    cudaStream_t s) {
+                    cudaStream_t s, int fylo = 0, int fyhi = -1) {
     if (t->kind == kP1) {
         const int nf1 = 2 * t->nc1 - 1;
-        const int m = t->nc1;
-        const dim3 g((nf1 + kTX - 1) / kTX, (m + kTY * kRPT - 1) / (kTY * kRPT));
+        if (fyhi < 0) fyhi = nf1;
+        const int crows = std::min(t->nc1, (fyhi + 1) >> 1) - (fylo >> 1);
+        if (crows <= 0) return;
+        const dim3 g((nf1 + kTX - 1) / kTX, (crows + kTY * kRPT - 1) / (kTY * kRPT));
         OCMG_LAUNCH(k_p1_prolong_add_tiled, g, dim3(kTX, kTY), 0, s, t->nc1,
-                    t->n_fields, c, xf);
+                    t->n_fields, c, xf, fylo, fyhi);
     } else {
         OCMG_LAUNCH(k_csr_spmv_add, grid_for(t->nf, kBlk), kBlk, 0, s, 
             t->nf, t->P.off.p, t->P.col.p, t->P.val.p, c, xf);
@@ -955,16 +967,46 @@ int ocmg_ne_gs_sweep_strip(const ocmg_level *lv, int forward, int y_begin,
         P.forward = forward ? 1 : 0;
         P.y_begin = y_begin;
         P.y_end = y_end;
-        P.fs_in = P.fs_out = (int64_t)(slab_end - slab_begin) * n1;
-        P.fs_x = (int64_t)(y_end - y_begin) * n1;
+        P.fs_in = P.fs_out = P.fs_x = (int64_t)(slab_end - slab_begin) * n1;
         std::copy(lv->mc_ci, lv->mc_ci + 58, &P.ci[0][0]);
         P.C = lv->mc_coef.p;
         P.rin = r_in - (int64_t)slab_begin * n1;
         P.rout = r_out - (int64_t)slab_begin * n1;
-        P.x = x - (int64_t)y_begin * n1;
+        P.x = x - (int64_t)slab_begin * n1;
         OCMG_LAUNCH(k_p1_mc_sweep, pl.grid, mcs::NT, mcs::SMEM, as_stream(stream), P);
         OCMG_LAUNCH_CHECK();
         if (ops) *ops = 2 * lv->nnz * (int64_t)(y_end - y_begin) / n1;
+    });
+}
+
+int ocmg_residual_rows(const ocmg_level *lv, const double *x, const double *f,
+                       double *r, int y_begin, int y_end, void *stream) {
+    return guarded([&] {
+        OCMG_REQUIRE(lv && x && r, "null argument");
+        OCMG_REQUIRE(lv->kind == kP1, "row ranges need a structured P1 level");
+        OCMG_REQUIRE(0 <= y_begin && y_begin <= y_end && y_end <= lv->n1, "bad rows");
+        level_residual(lv, x, f, r, as_stream(stream), y_begin, y_end);
+    });
+}
+
+int ocmg_restrict_rows(const ocmg_transfer *t, const double *rf, double *rc,
+                       int cy_begin, int cy_end, void *stream) {
+    return guarded([&] {
+        OCMG_REQUIRE(t && rf && rc, "null argument");
+        OCMG_REQUIRE(t->kind == kP1, "row ranges need a structured P1 transfer");
+        OCMG_REQUIRE(0 <= cy_begin && cy_begin <= cy_end && cy_end <= t->nc1, "bad rows");
+        do_restrict(t, rf, rc, as_stream(stream), cy_begin, cy_end);
+    });
+}
+
+int ocmg_prolong_add_rows(const ocmg_transfer *t, const double *c, double *xf,
+                          int fy_begin, int fy_end, void *stream) {
+    return guarded([&] {
+        OCMG_REQUIRE(t && c && xf, "null argument");
+        OCMG_REQUIRE(t->kind == kP1, "row ranges need a structured P1 transfer");
+        OCMG_REQUIRE(0 <= fy_begin && fy_begin <= fy_end && fy_end <= 2 * t->nc1 - 1,
+                     "bad rows");
+        do_prolong_add(t, c, xf, as_stream(stream), fy_begin, fy_end);
     });
 }
 

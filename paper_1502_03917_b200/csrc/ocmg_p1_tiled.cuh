@@ -122,12 +122,14 @@ __device__ __forceinline__ void p1_residual_rows(const P1Coef28 &A, int64_t N,
 __global__ void __launch_bounds__(kTX *kTY)
     k_p1_residual_int(int n1, const __grid_constant__ P1Coef28 A,
                       const double *__restrict__ x, const double *__restrict__ f,
-                      double *__restrict__ r) {
+                      double *__restrict__ r, int ylo, int yhi) {
+    // interior columns and rows, restricted to the rows [ylo, yhi)
     const int lo = kRing, hi = n1 - 1 - kRing;
+    const int rlo = max(lo, ylo), rhi = min(hi, yhi - 1);
     const int ix = lo + blockIdx.x * kTX + threadIdx.x;
-    const int iy0 = lo + (blockIdx.y * kTY + threadIdx.y) * kRPT;
-    if (ix > hi || iy0 > hi) return;
-    const int nrows = min(kRPT, hi - iy0 + 1);
+    const int iy0 = rlo + (blockIdx.y * kTY + threadIdx.y) * kRPT;
+    if (ix > hi || iy0 > rhi) return;
+    const int nrows = min(kRPT, rhi - iy0 + 1);
     const int64_t N = (int64_t)n1 * n1, v0 = (int64_t)iy0 * n1 + ix;
     if (nrows == kRPT)
         p1_residual_rows<kRPT>(A, N, n1, v0, x, f, r, nrows);
@@ -138,10 +140,10 @@ __global__ void __launch_bounds__(kTX *kTY)
 __global__ void k_p1_residual_ring(int n1, const double *__restrict__ T,
                                    const double *__restrict__ x,
                                    const double *__restrict__ f,
-                                   double *__restrict__ r) {
+                                   double *__restrict__ r, int ylo, int yhi) {
     int ix, iy;
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (!p1_ring_node(k, n1, kRing, ix, iy)) return;
+    if (!p1_ring_node(k, n1, kRing, ix, iy) || iy < ylo || iy >= yhi) return;
     const int64_t N = (int64_t)n1 * n1;
     const P1Node q = p1_node(ix, iy, n1);
     const double *A = T + kP1OffA + q.c * 28;
@@ -317,11 +319,12 @@ __global__ void k_p1_ne_apply_ring(int n1, const double *__restrict__ T,
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kTX *kTY)
     k_p1_restrict_tiled(int nc1, int n_fields, const double *__restrict__ rf,
-                        double *__restrict__ rc) {
+                        double *__restrict__ rc, int cylo, int cyhi) {
+    // coarse rows [cylo, cyhi)
     const int cx = blockIdx.x * kTX + threadIdx.x;
-    const int cy0 = (blockIdx.y * kTY + threadIdx.y) * kRPT;
-    if (cx >= nc1 || cy0 >= nc1) return;
-    const int nrows = min(kRPT, nc1 - cy0);
+    const int cy0 = cylo + (blockIdx.y * kTY + threadIdx.y) * kRPT;
+    if (cx >= nc1 || cy0 >= cyhi) return;
+    const int nrows = min(kRPT, cyhi - cy0);
     const int nf1 = 2 * nc1 - 1;
     const int64_t Nc = (int64_t)nc1 * nc1, Nf = (int64_t)nf1 * nf1;
     const bool l = cx > 0, rr = cx < nc1 - 1;
@@ -370,14 +373,16 @@ __global__ void __launch_bounds__(kTX *kTY)
 // vertices copy (1.0*c), edge midpoints average their two ends (lower first)
 __global__ void __launch_bounds__(kTX *kTY)
     k_p1_prolong_add_tiled(int nc1, int n_fields, const double *__restrict__ c,
-                           double *__restrict__ xf) {
+                           double *__restrict__ xf, int fylo, int fyhi) {
+    // fine rows [fylo, fyhi), walked as coarse rows [fylo/2, (fyhi+1)/2)
     const int nf1 = 2 * nc1 - 1;
     const int fx = blockIdx.x * kTX + threadIdx.x;
-    const int cy0 = (blockIdx.y * kTY + threadIdx.y) * kRPT;  // coarse rows
-    if (fx >= nf1 || cy0 >= nc1) return;
+    const int cylo = fylo >> 1, cyhi = min(nc1, (fyhi + 1) >> 1);
+    const int cy0 = cylo + (blockIdx.y * kTY + threadIdx.y) * kRPT;  // coarse rows
+    if (fx >= nf1 || cy0 >= cyhi) return;
     const int64_t Nc = (int64_t)nc1 * nc1, Nf = (int64_t)nf1 * nf1;
     const int ox = fx & 1, hx = fx >> 1;
-    const int cend = min(cy0 + kRPT, nc1);
+    const int cend = min(cy0 + kRPT, cyhi);
     for (int b = 0; b < n_fields; ++b) {
         const double *cc = c + b * Nc;
         double *xb = xf + b * Nf;
@@ -389,7 +394,7 @@ __global__ void __launch_bounds__(kTX *kTY)
 #pragma unroll 4
         for (int cy = cy0; cy < cend; ++cy) {
             const int64_t fv = (int64_t)(2 * cy) * nf1 + fx;
-            xb[fv] = __dadd_rn(xb[fv], lo);
+            if (2 * cy >= fylo && 2 * cy < fyhi) xb[fv] = __dadd_rn(xb[fv], lo);
             if (cy + 1 < nc1) {
                 const double *qn = cc + (int64_t)(cy + 1) * nc1 + hx;
                 const double a_hi = __ldg(qn), b_hi = ox ? __ldg(qn + 1) : 0.0;
@@ -397,7 +402,8 @@ __global__ void __launch_bounds__(kTX *kTY)
                 // (ox=1) diagonal edge (hx,cy)-(hx+1,cy+1)
                 const double mid = ox ? __dadd_rn(__dmul_rn(0.5, a_lo), __dmul_rn(0.5, b_hi))
                                       : __dadd_rn(__dmul_rn(0.5, a_lo), __dmul_rn(0.5, a_hi));
-                xb[fv + nf1] = __dadd_rn(xb[fv + nf1], mid);
+                if (2 * cy + 1 >= fylo && 2 * cy + 1 < fyhi)
+                    xb[fv + nf1] = __dadd_rn(xb[fv + nf1], mid);
                 lo = ox ? __dadd_rn(__dmul_rn(0.5, a_hi), __dmul_rn(0.5, b_hi))
                         : __dmul_rn(1.0, a_hi);
                 a_lo = a_hi;

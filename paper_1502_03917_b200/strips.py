@@ -124,17 +124,20 @@ class LoopbackExchange:
                 slab[:, c:d].copy_(slabs[peer][:, rows])
 
 
-def strip_sweep(system, part, x_own, r_in, r_out, forward=True, stream=None):
+def strip_sweep(system, part, x, r_in, r_out, forward=True, stream=None):
     """One multicolour NE-GS sweep of this rank's strip (ghosts of r_in must
-    be current).  system: the structured level (every rank builds the same
-    level handle; only its coefficient tables are used)."""
+    be current).  x, r_in, r_out: slabs (2, slab_rows, n1) -- or full-size
+    level vectors with part.s0 = 0, part.s1 = n1 (see StripMultigrid).
+    system: the structured level (every rank builds the same level handle;
+    only its coefficient tables are used)."""
     n1 = part.n1
-    if x_own.shape != (2, part.rows, n1) or r_in.shape != (2, part.slab_rows, n1) \
-            or r_out.shape != r_in.shape:
-        raise ValueError("strip tensors have the wrong shape")
+    shape = (2, part.s1 - part.s0, n1)
+    for t in (x, r_in, r_out):
+        if tuple(t.reshape(2, -1, n1).shape) != shape:
+            raise ValueError("strip tensors have the wrong shape")
     ops = ctypes.c_int64()
     _lib.call("ocmg_ne_gs_sweep_strip", system.handle, 1 if forward else 0,
-              part.y0, part.y1, part.s0, part.s1, _lib.dptr(x_own),
+              part.y0, part.y1, part.s0, part.s1, _lib.dptr(x),
               _lib.dptr(r_in), _lib.dptr(r_out),
               stream if stream is not None else _lib.stream_ptr(),
               ctypes.byref(ops))
@@ -153,11 +156,286 @@ class StripSmoother:
         self.spare = torch.empty((2, part.slab_rows, part.n1),
                                  dtype=torch.float64, device="cuda")
 
-    def sweep(self, x_own, r_slab, forward=True):
+    def sweep(self, x_slab, r_slab, forward=True):
         """Returns the slab holding the new residual (r_slab or the spare;
         the other becomes the spare)."""
         exchange_ghosts(r_slab, self.part, self.group)
         out = self.spare
-        strip_sweep(self.system, self.part, x_own, r_slab, out, forward)
+        strip_sweep(self.system, self.part, x_slab, r_slab, out, forward)
         self.spare = r_slab
         return out
+
+
+# ---------------------------------------------------------------------------
+# Strip-partitioned multigrid cycle (Poisson control, multicolour NE-GS)
+# ---------------------------------------------------------------------------
+
+def nested_bounds(n1_levels, world_size, ghost=GHOST):
+    """Row bounds per rank for a coarse-to-fine list of grid sizes, nested
+    (fine strip [2 y0, 2 y1), the last clipped to n1): a coarse row and the
+    fine rows it restricts from live on the same rank.  Returns (first
+    partitioned index, bounds per level) -- levels below stay whole."""
+    first = None
+    for i, n1 in enumerate(n1_levels):
+        if n1 // world_size >= ghost:
+            first = i
+            break
+    if first is None:
+        raise ValueError("no level is wide enough to split over "
+                         f"{world_size} ranks")
+    bounds = [None] * len(n1_levels)
+    base = StripPartition(n1_levels[first], world_size, 0, ghost).bounds
+    bounds[first] = base
+    for i in range(first + 1, len(n1_levels)):
+        n1 = n1_levels[i]
+        bounds[i] = [(2 * a, min(2 * b, n1)) for a, b in bounds[i - 1]]
+        bounds[i][-1] = (bounds[i][-1][0], n1)
+    return first, bounds
+
+
+def _rows(v, n1, a, b):
+    """Per-field contiguous views of the rows [a, b) of a full-size level
+    vector (2 n1^2,)."""
+    N = n1 * n1
+    return [v[f * N + a * n1:f * N + b * n1] for f in range(2)]
+
+
+class LoopbackComm:
+    """Every rank's state in this process: exchanges are copies.  Lets one
+    GPU run the partitioned cycle rank after rank and compare it with the
+    single-GPU cycle (no kernel ever waits on another rank)."""
+
+    def exchange(self, states, level, name, g):
+        for st in states:
+            y0, y1 = st.bounds[level]
+            n1 = st.n1[level]
+            v = getattr(st, name)[level]
+            for peer in (st.rank - 1, st.rank + 1):
+                if 0 <= peer < len(states):
+                    a, b = (y0 - g, y0) if peer < st.rank else (y1, y1 + g)
+                    src = getattr(states[peer], name)[level]
+                    for dst_f, src_f in zip(_rows(v, n1, a, b), _rows(src, n1, a, b)):
+                        dst_f.copy_(src_f)
+
+    def allgather(self, states, level, name):
+        for st in states:
+            v = getattr(st, name)[level]
+            n1 = st.n1[level]
+            for peer in states:
+                if peer is st:
+                    continue
+                a, b = peer.bounds[level]
+                src = getattr(peer, name)[level]
+                for dst_f, src_f in zip(_rows(v, n1, a, b), _rows(src, n1, a, b)):
+                    dst_f.copy_(src_f)
+
+    def allreduce(self, values):
+        total = sum(values)
+        return [total] * len(values)
+
+
+class DistComm:
+    """One rank per process, torch.distributed (NCCL over NVLink for CUDA
+    tensors): ghost rows by isend/irecv straight into the full-size vectors,
+    all-gather by one broadcast per rank and field, sums by all_reduce."""
+
+    def __init__(self, group=None, device="cuda"):
+        self.group, self.device = group, device
+
+    def exchange(self, states, level, name, g):
+        import torch.distributed as dist
+        (st,) = states
+        y0, y1 = st.bounds[level]
+        n1 = st.n1[level]
+        v = getattr(st, name)[level]
+        reqs = []
+        for peer in (st.rank - 1, st.rank + 1):
+            if not 0 <= peer < st.world_size:
+                continue
+            snd = (y0, y0 + g) if peer < st.rank else (y1 - g, y1)
+            rcv = (y0 - g, y0) if peer < st.rank else (y1, y1 + g)
+            for s_f, r_f in zip(_rows(v, n1, *snd), _rows(v, n1, *rcv)):
+                reqs.append(dist.isend(s_f, peer, group=self.group))
+                reqs.append(dist.irecv(r_f, peer, group=self.group))
+        for r in reqs:
+            r.wait()
+
+    def allgather(self, states, level, name):
+        import torch.distributed as dist
+        (st,) = states
+        v = getattr(st, name)[level]
+        n1 = st.n1[level]
+        for p in range(st.world_size):
+            a, b = st.all_bounds[level][p]
+            for f_view in _rows(v, n1, a, b):
+                dist.broadcast(f_view, p, group=self.group)
+
+    def allreduce(self, values):
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor(values, dtype=torch.float64, device=self.device)
+        dist.all_reduce(t, group=self.group)
+        return t.tolist()
+
+
+class _RankState:
+    def __init__(self, rank, world_size, n1s, all_bounds, first, device="cuda"):
+        import torch
+        self.rank, self.world_size = rank, world_size
+        self.n1 = n1s
+        self.all_bounds = all_bounds
+        self.bounds = [b[rank] if b is not None else None for b in all_bounds]
+
+        def vec(i):
+            return torch.zeros(2 * n1s[i] ** 2, dtype=torch.float64, device=device)
+        L = len(n1s)
+        # x, f on every level from the gather level up; r, r2 where smoothed
+        self.x = [vec(i) if i >= first - 1 else None for i in range(L)]
+        self.f = [vec(i) if i >= first - 1 else None for i in range(L)]
+        # (bounds[first-1] are the gathered level's rows this rank restricts)
+        self.r = [vec(i) if i >= first else None for i in range(L)]
+        self.r2 = [vec(i) if i >= first else None for i in range(L)]
+
+
+class StripMultigrid:
+    """The BASELINE V/W cycle with its fine levels split into row strips
+    (SURVEY.md §8(e)).  Levels whose strips would be thinner than the 29
+    ghost rows of a sweep are gathered: every rank runs the same single-GPU
+    sub-cycle on them (ocmg_cycle of the hierarchy topped there).
+
+    Per partitioned level visit: x ghost (1 row) -> residual rows; per sweep
+    r ghost (29 rows) -> strip sweep (residual ping-pong); r ghost (1 row) ->
+    restriction rows; coarse visit(s); coarse x ghost (1 row) -> prolongation
+    rows; residual; post-sweeps.  Every row is computed with the single-GPU
+    kernels' arithmetic, so the iterate is bit-identical to Multigrid's.
+
+    mg: a Poisson Multigrid with gs_mode="multicolour" (it supplies the
+    levels, transfers and the gathered sub-hierarchy).  ranks: the ranks
+    this process drives (one with DistComm; all of them with LoopbackComm).
+    """
+
+    def __init__(self, mg, world_size, ranks, comm):
+        cfg = mg.config
+        if cfg.gs_mode != "multicolour" or cfg.smoother.name not in ("lsgs", "slsgs"):
+            raise ValueError("strip cycles run multicolour NE-GS smoothers")
+        if not all(getattr(s, "structured", False) for s in mg.systems[1:]):
+            raise ValueError("strip cycles need structured Poisson levels")
+        self.mg, self.comm = mg, comm
+        n1s = [2 ** s.level + 1 for s in mg.systems]
+        first, bounds = nested_bounds(n1s, world_size)
+        if first < 2:
+            raise ValueError("partitioned levels must leave a gathered "
+                             "sub-hierarchy of at least one smoothed level")
+        self.first, self.gather = first, first - 1
+        # each rank restricts the gathered level's rows that its fine strip
+        # covers: coarse row c reads fine rows 2c-1 .. 2c+1 (one ghost row)
+        bounds[first - 1] = [((a + 1) // 2, (b + 1) // 2) for a, b in bounds[first]]
+        self.n1s = n1s
+        self.states = [_RankState(r, world_size, n1s, bounds, first) for r in ranks]
+        self.w = cfg.cycle == "w"
+        self.nu_pre, self.nu_post = cfg.nu_pre, cfg.nu_post
+        self.slsgs = cfg.smoother.name == "slsgs"
+
+    # -- per-level operations on every driven rank --------------------------
+    def _resid(self, i):
+        self.comm.exchange(self.states, i, "x", 1)
+        sysi = self.mg.systems[i]
+        for st in self.states:
+            y0, y1 = st.bounds[i]
+            _lib.call("ocmg_residual_rows", sysi.handle, _lib.dptr(st.x[i]),
+                      _lib.dptr(st.f[i]), _lib.dptr(st.r[i]), y0, y1,
+                      _lib.stream_ptr())
+
+    def _sweep(self, i, forward):
+        self.comm.exchange(self.states, i, "r", GHOST)
+        sysi = self.mg.systems[i]
+        n1 = self.n1s[i]
+        for st in self.states:
+            y0, y1 = st.bounds[i]
+            ops = ctypes.c_int64()
+            _lib.call("ocmg_ne_gs_sweep_strip", sysi.handle, 1 if forward else 0,
+                      y0, y1, 0, n1, _lib.dptr(st.x[i]), _lib.dptr(st.r[i]),
+                      _lib.dptr(st.r2[i]), _lib.stream_ptr(), ctypes.byref(ops))
+            st.r[i], st.r2[i] = st.r2[i], st.r[i]
+
+    def _smooth(self, i, nu):
+        for _ in range(nu):
+            self._sweep(i, True)
+            if self.slsgs:
+                self._sweep(i, False)
+
+    def _visit(self, i):
+        if i == self.gather:
+            self.comm.allgather(self.states, i, "f")
+            for st in self.states:
+                self.mg.cycle(i, st.x[i], st.f[i])
+            return
+        self._resid(i)
+        self._smooth(i, self.nu_pre)
+        self.comm.exchange(self.states, i, "r", 1)
+        t = self.mg.transfers[i - 1]
+        for st in self.states:
+            cy0, cy1 = st.bounds[i - 1]
+            _lib.call("ocmg_restrict_rows", t.handle, _lib.dptr(st.r[i]),
+                      _lib.dptr(st.f[i - 1]), cy0, cy1, _lib.stream_ptr())
+            st.x[i - 1].zero_()
+        rec = 2 if (self.w and i - 1 > 0) else 1
+        for _ in range(rec):
+            self._visit(i - 1)
+        if i - 1 >= self.first:
+            self.comm.exchange(self.states, i - 1, "x", 1)
+        for st in self.states:
+            fy0, fy1 = st.bounds[i]
+            _lib.call("ocmg_prolong_add_rows", t.handle, _lib.dptr(st.x[i - 1]),
+                      _lib.dptr(st.x[i]), fy0, fy1, _lib.stream_ptr())
+        self._resid(i)
+        self._smooth(i, self.nu_post)
+
+    def cycle(self):
+        self._visit(len(self.n1s) - 1)
+
+    def load(self, f_full, x_full=None):
+        """Copy the finest rhs (and start vector) rows into the rank states
+        (f_full / x_full: full-size device vectors)."""
+        top = len(self.n1s) - 1
+        for st in self.states:
+            st.f[top].copy_(f_full)
+            if x_full is None:
+                st.x[top].zero_()
+            else:
+                st.x[top].copy_(x_full)
+
+    def gather_x(self):
+        """The finest iterate assembled from the ranks' own rows (loopback)."""
+        import torch
+        top = len(self.n1s) - 1
+        n1 = self.n1s[top]
+        out = torch.empty_like(self.states[0].x[top])
+        for st in self.states:
+            y0, y1 = st.bounds[top]
+            for o, s in zip(_rows(out, n1, y0, y1), _rows(st.x[top], n1, y0, y1)):
+                o.copy_(s)
+        return out
+
+    def solve(self, tol=1e-8, max_cycles=300):
+        """BASELINE protocol on the partition: rel = ||f - A x|| / ||f||
+        from the ranks' own rows (all_reduce), stop at tol."""
+        top = len(self.n1s) - 1
+        n1 = self.n1s[top]
+
+        def own_sumsq(vecs):
+            vals = []
+            for st, v in zip(self.states, vecs):
+                y0, y1 = st.bounds[top]
+                vals.append(float(sum((t * t).sum() for t in _rows(v, n1, y0, y1))))
+            return self.comm.allreduce(vals)[0]
+        fn = own_sumsq([st.f[top] for st in self.states]) ** 0.5
+        hist = []
+        for _ in range(max_cycles):
+            self.cycle()
+            self._resid(top)
+            rel = own_sumsq([st.r[top] for st in self.states]) ** 0.5 / fn
+            hist.append(rel)
+            if rel <= tol:
+                break
+        return hist

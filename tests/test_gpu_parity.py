@@ -248,7 +248,7 @@ def test_strip_sweeps_match_single_gpu(k, ws):
     x = torch.rand(dsys.n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
     r = torch.rand(dsys.n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
     parts = [StripPartition(n1, ws, p) for p in range(ws)]
-    xs = [p.scatter_own(x) for p in parts]
+    xs = [p.scatter(x) for p in parts]
     rs = [p.scatter(r) for p in parts]
     outs = [torch.empty_like(t) for t in rs]
     lb = LoopbackExchange(parts)
@@ -260,7 +260,7 @@ def test_strip_sweeps_match_single_gpu(k, ws):
             strip_sweep(dsys, p, xo, ri, ro, forward=fwd)
         rs, outs = outs, rs
     torch.cuda.synchronize()
-    xg = torch.cat([xo for xo in xs], dim=1).reshape(-1)
+    xg = torch.cat([p.own(xo) for p, xo in zip(parts, xs)], dim=1).reshape(-1)
     rg = torch.cat([p.own(ri) for p, ri in zip(parts, rs)], dim=1).reshape(-1)
     assert torch.equal(xg, x)
     assert torch.equal(rg, r)
@@ -286,6 +286,27 @@ def test_fused_coarse_block_is_bit_identical(cycle, smoother, k):
         hs.append(hist)
     assert np.array_equal(xs[0], xs[1])
     assert hs[0] == hs[1]
+
+
+@pytest.mark.parametrize("k,ws,cycle,smoother", [(8, 2, "v", "lsgs"),
+                                                  (9, 4, "w", "lsgs"),
+                                                  (9, 3, "v", "slsgs")])
+def test_strip_multigrid_matches_single_gpu(k, ws, cycle, smoother):
+    """The strip-partitioned cycle, every rank run in this
+    process with loopback exchanges, reproduces the single-GPU cycle bit for
+    bit; the stopping norms agree to rounding."""
+    from paper_1502_03917_b200.strips import LoopbackComm, StripMultigrid
+    cfg = P.CycleConfig(smoother=P.SmootherKind(smoother), cycle=cycle,
+                        coarsest_level=3, gs_mode="multicolour")
+    mg = P.build_solver("poisson", k, 1e-6, cfg)
+    f = P.baseline_rhs(mg.finest, 0, add_sine=True)
+    x1, h1 = mg.solve_to_tolerance(f, tol=0.0, max_cycles=3)
+    sm = StripMultigrid(mg, ws, list(range(ws)), LoopbackComm())
+    sm.load(f)
+    h2 = sm.solve(tol=0.0, max_cycles=3)
+    torch.cuda.synchronize()
+    assert torch.equal(sm.gather_x(), x1)
+    assert np.allclose(h1, h2, rtol=1e-12, atol=0)
 
 
 @pytest.mark.parametrize("prob,kc", [("poisson", 1), ("poisson", 4),

@@ -79,3 +79,75 @@ def test_gloo_ghost_exchange(ws):
     for p in procs:
         p.join(timeout=60)
     assert res == {r: True for r in range(ws)}, res
+
+
+def _dist_comm_worker(rank, ws, port, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=ws)
+        from paper_1502_03917_b200.strips import DistComm, _RankState, nested_bounds
+        n1s = [17, 33, 65, 129]
+        first, bounds = nested_bounds(n1s, ws)
+        bounds[first - 1] = [((a + 1) // 2, (b + 1) // 2) for a, b in bounds[first]]
+        st = _RankState(rank, ws, n1s, bounds, first, device="cpu")
+        comm = DistComm(device="cpu")
+        ok = True
+        # ghost exchange on the finest level: own rows hold the global index
+        top = len(n1s) - 1
+        n1 = n1s[top]
+        glob = torch.arange(2 * n1 * n1, dtype=torch.float64)
+        y0, y1 = st.bounds[top]
+        for fld in range(2):
+            a, b = fld * n1 * n1 + y0 * n1, fld * n1 * n1 + y1 * n1
+            st.x[top][a:b] = glob[a:b]
+        comm.exchange([st], top, "x", 2)
+        for fld in range(2):
+            lo = max(0, y0 - 2) * n1 + fld * n1 * n1
+            hi = min(n1, y1 + 2) * n1 + fld * n1 * n1
+            ok &= torch.equal(st.x[top][lo:hi], glob[lo:hi])
+        # all-gather of the gathered level's contributions
+        g = first - 1
+        c0, c1 = st.bounds[g]
+        m = n1s[g]
+        for fld in range(2):
+            a, b = fld * m * m + c0 * m, fld * m * m + c1 * m
+            st.f[g][a:b] = torch.arange(a, b, dtype=torch.float64)
+        comm.allgather([st], g, "f")
+        ok &= torch.equal(st.f[g], torch.arange(2 * m * m, dtype=torch.float64))
+        s = comm.allreduce([float(rank + 1)])
+        ok &= s[0] == ws * (ws + 1) / 2
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, bool(ok)))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+
+
+def test_gloo_dist_comm_exchange_gather_reduce():
+    ws = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dist_comm_worker, args=(r, ws, port, q))
+             for r in range(ws)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(ws))
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {r: True for r in range(ws)}, res
+
+
+def test_nested_bounds_tile_and_nest():
+    from paper_1502_03917_b200.strips import nested_bounds
+    n1s = [2 ** k + 1 for k in range(3, 13)]
+    for ws in (2, 4, 8):
+        first, b = nested_bounds(n1s, ws)
+        assert n1s[first] // ws >= GHOST and n1s[first - 1] // ws < GHOST
+        for i in range(first, len(n1s)):
+            assert b[i][0][0] == 0 and b[i][-1][1] == n1s[i]
+            assert all(p[1] == q[0] for p, q in zip(b[i], b[i][1:]))
+            assert min(y1 - y0 for y0, y1 in b[i]) >= GHOST
+            if i > first:
+                assert all(f[0] == 2 * c[0] for f, c in zip(b[i], b[i - 1]))
