@@ -241,13 +241,16 @@ def kernel_table(dsys, coarse_sys, transfer, x, r, f, stream, iters, hbm):
     return rows
 
 
-def solve_timing(level, alpha, cycle, coarsest, mode, sine, problem="poisson"):
+def solve_timing(level, alpha, cycle, coarsest, mode, sine, problem="poisson",
+                 smoother="lsgs"):
     """Time to 1e-8 relative residual (BASELINE protocol), setup excluded."""
     import torch
 
     import paper_1502_03917_b200 as P
     t_setup = time.perf_counter()
-    cfg = P.CycleConfig(smoother=P.SmootherKind("lsgs"), cycle=cycle,
+    kind = (P.SmootherKind("normal", tau=0.4) if smoother == "normal"
+            else P.SmootherKind(smoother))
+    cfg = P.CycleConfig(smoother=kind, cycle=cycle,
                         coarsest_level=coarsest, gs_mode=mode)
     mg = P.build_solver(problem, level, alpha, cfg)
     f = P.baseline_rhs(mg.finest, 0 if problem == "poisson" else 1,
@@ -260,8 +263,9 @@ def solve_timing(level, alpha, cycle, coarsest, mode, sine, problem="poisson"):
     _, hist = mg.solve_to_tolerance(f, tol=1e-8, max_cycles=300)
     torch.cuda.synchronize()
     t = time.perf_counter() - t0
+    sm_name = "NE-Jacobi(tau=0.4)" if smoother == "normal" else f"NE-GS[{mode}]"
     return {"config": f"{problem} L{level} alpha={alpha} {cycle.upper()}(2,2) "
-                      f"NE-GS[{mode}] coarsest L{coarsest}"
+                      f"{sm_name} coarsest L{coarsest}"
                       + (" y_D=U+sin*sin" if sine else ""),
             "cycles": len(hist), "final_rel_residual": hist[-1],
             "convergence_factor": float(hist[-1] ** (1.0 / len(hist))),
@@ -498,8 +502,13 @@ def run_gpu_arm(args, ws, rank, local):
             st_o.sweep(x, r)
             t_o = time_events(lambda: st_o.sweep(x, r), 3, stream)
             result["modes"][other] = {"dof_per_s": n / t_o, "ms": t_o * 1e3}
-            result["solve"] = [solve_timing(10, 1e-4, "v", 2, m, False)
-                               for m in ("multicolour", "wavefront")]
+            # config 2: L10, NE-GS (both modes) vs NE-Jacobi, three alphas
+            result["solve"] = []
+            for a in (1.0, 1e-4, 1e-8):
+                result["solve"] += [solve_timing(10, a, "v", 2, m, False)
+                                    for m in ("wavefront", "multicolour")]
+                result["solve"].append(solve_timing(10, a, "v", 2, "wavefront",
+                                                    False, smoother="normal"))
             # Stokes control (configs 4 and 5; generic CSR kernels)
             result["solve"] += [solve_timing(5, 1e-4, "v", 1, m, False, "stokes")
                                 for m in ("wavefront", "multicolour")]
