@@ -268,7 +268,8 @@ void level_ne_jacobi(const ocmg_level *lv, double tau, double *x, double *r,
         OCMG_LAUNCH(k_p1_ne_p_int, g, b, 0, s, lv->n1, C, r, scratch);
         OCMG_LAUNCH(k_p1_ne_p_ring, grid_for(nring, kBlk), kBlk, 0, s, lv->n1,
                     lv->tables.p, tau, r, scratch);
-        OCMG_LAUNCH(k_p1_ne_apply_int, g, b, 0, s, lv->n1, lv->cA, scratch, x, r);
+        const dim3 ga(g.x, (lv->n1 - 2 * kRing + kTY * (kRPT / 2) - 1) / (kTY * (kRPT / 2)));
+        OCMG_LAUNCH(k_p1_ne_apply_int, ga, b, 0, s, lv->n1, lv->cA, scratch, x, r);
         OCMG_LAUNCH(k_p1_ne_apply_ring, grid_for(nring, kBlk), kBlk, 0, s, lv->n1,
                     lv->tables.p, scratch, x, r);
     } else {

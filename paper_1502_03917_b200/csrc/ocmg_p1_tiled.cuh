@@ -224,13 +224,26 @@ __global__ void k_p1_ne_p_ring(int n1, const double *__restrict__ T, double tau,
 // ---------------------------------------------------------------------------
 // NE-Jacobi phase 2: x += p; r_j -= sum_i A_ji p_i (CSR order of row j)
 // ---------------------------------------------------------------------------
-template <int NR>
+template <int NR, bool FULL>
 __device__ __forceinline__ void p1_neapply_rows(const P1Coef28 &A, int64_t N,
                                                 int n1, int64_t v0,
                                                 const double *__restrict__ p,
                                                 double *__restrict__ x,
                                                 double *__restrict__ r,
                                                 int nrows) {
+    // x and r of all rows first: the compiler cannot prove that row j+1's
+    // loads miss row j's stores (same arrays), so interleaving them would
+    // expose one HBM round trip per row
+    double xo[NR][2], ro[NR][2];
+#pragma unroll
+    for (int j = 0; j < NR; ++j)
+        if (FULL || j < nrows)
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+                const int64_t i = b * N + v0 + (int64_t)j * n1;
+                xo[j][b] = x[i];
+                ro[j][b] = r[i];
+            }
     double w[2][3][3];
 #pragma unroll
     for (int b = 0; b < 2; ++b) {
@@ -239,7 +252,7 @@ __device__ __forceinline__ void p1_neapply_rows(const P1Coef28 &A, int64_t N,
     }
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
-        if (NR == kRPT || j < nrows) {
+        if (FULL || j < nrows) {
             const int64_t v = v0 + (int64_t)j * n1;
 #pragma unroll
             for (int b = 0; b < 2; ++b) p1_load_row(p + b * N + v + n1, w[b][2]);
@@ -248,8 +261,8 @@ __device__ __forceinline__ void p1_neapply_rows(const P1Coef28 &A, int64_t N,
 #pragma unroll
             for (int b = 0; b < 2; ++b) {
                 const int64_t i = b * N + v;
-                x[i] = __dadd_rn(x[i], w[b][1][1]);
-                double ri = r[i];
+                x[i] = __dadd_rn(xo[j][b], w[b][1][1]);
+                double ri = ro[j][b];
 #pragma unroll
                 for (int d = 0; d < 7; ++d)
                     ri = __dsub_rn(ri, __dmul_rn(A.c[14 * b + d], s[d]));
@@ -273,16 +286,18 @@ __global__ void __launch_bounds__(kTX *kTY)
     k_p1_ne_apply_int(int n1, const __grid_constant__ P1Coef28 A,
                       const double *__restrict__ p, double *__restrict__ x,
                       double *__restrict__ r) {
+    // 4 rows per thread here: the x/r preload of 8 rows cost occupancy
+    constexpr int R = kRPT / 2;
     const int lo = kRing, hi = n1 - 1 - kRing;
     const int ix = lo + blockIdx.x * kTX + threadIdx.x;
-    const int iy0 = lo + (blockIdx.y * kTY + threadIdx.y) * kRPT;
+    const int iy0 = lo + (blockIdx.y * kTY + threadIdx.y) * R;
     if (ix > hi || iy0 > hi) return;
-    const int nrows = min(kRPT, hi - iy0 + 1);
+    const int nrows = min(R, hi - iy0 + 1);
     const int64_t N = (int64_t)n1 * n1, v0 = (int64_t)iy0 * n1 + ix;
-    if (nrows == kRPT)
-        p1_neapply_rows<kRPT>(A, N, n1, v0, p, x, r, nrows);
+    if (nrows == R)
+        p1_neapply_rows<R, true>(A, N, n1, v0, p, x, r, nrows);
     else
-        p1_neapply_rows<kRPT - 1>(A, N, n1, v0, p, x, r, nrows);
+        p1_neapply_rows<R, false>(A, N, n1, v0, p, x, r, nrows);
 }
 
 __global__ void k_p1_ne_apply_ring(int n1, const double *__restrict__ T,

@@ -26,7 +26,7 @@ _lib.check(fn(s.handle, buf.ctypes.data_as(ctypes.c_void_p), dims))
 t = buf.reshape(nb, niter, nw, 2).astype(np.int64)
 t0 = t[t > 0].min()
 t = t - t0
-names = ["chain1", "chain2+scout", "G1a", "G1b", "u0", "u1", "G2a", "G2b", "r0", "r1"]
+names = ["chain1", "chain2", "scout"] + [f"{s}{i}" for s in ("G1_", "u_", "G2_", "r_") for i in range(4)]
 print(f"k={k} nb={nb} niter={niter} total {(t.max())/1e3:.1f} us")
 for b in (0, nb // 2, nb - 1):
     dur = t[b, :, :, 1] - t[b, :, :, 0]
