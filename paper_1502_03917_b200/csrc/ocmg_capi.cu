@@ -579,8 +579,12 @@ void do_prolong_add(const ocmg_transfer *t, const double *c, double *xf,
         const int crows = std::min(t->nc1, (fyhi + 1) >> 1) - (fylo >> 1);
         if (crows <= 0) return;
         const dim3 g((nf1 + kTX - 1) / kTX, (crows + kTY * kRPT - 1) / (kTY * kRPT));
-        OCMG_LAUNCH(k_p1_prolong_add_tiled, g, dim3(kTX, kTY), 0, s, t->nc1,
-                    t->n_fields, c, xf, fylo, fyhi);
+        if (fylo == 0 && fyhi == nf1)
+            OCMG_LAUNCH(k_p1_prolong_add_tiled<true>, g, dim3(kTX, kTY), 0, s, t->nc1,
+                        t->n_fields, c, xf, fylo, fyhi);
+        else
+            OCMG_LAUNCH(k_p1_prolong_add_tiled<false>, g, dim3(kTX, kTY), 0, s, t->nc1,
+                        t->n_fields, c, xf, fylo, fyhi);
     } else {
         OCMG_LAUNCH(k_csr_spmv_add, grid_for(t->nf, kBlk), kBlk, 0, s, 
             t->nf, t->P.off.p, t->P.col.p, t->P.val.p, c, xf);

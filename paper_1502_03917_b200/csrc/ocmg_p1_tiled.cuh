@@ -386,6 +386,7 @@ __global__ void __launch_bounds__(kTX *kTY)
 
 // Prolongation x_f += P c: thread = fine column, 2*kRPT fine rows; even/even
 // vertices copy (1.0*c), edge midpoints average their two ends (lower first)
+template <bool ALL>  // ALL: the whole level (no row-range guards)
 __global__ void __launch_bounds__(kTX *kTY)
     k_p1_prolong_add_tiled(int nc1, int n_fields, const double *__restrict__ c,
                            double *__restrict__ xf, int fylo, int fyhi) {
@@ -409,7 +410,7 @@ __global__ void __launch_bounds__(kTX *kTY)
 #pragma unroll 4
         for (int cy = cy0; cy < cend; ++cy) {
             const int64_t fv = (int64_t)(2 * cy) * nf1 + fx;
-            if (2 * cy >= fylo && 2 * cy < fyhi) xb[fv] = __dadd_rn(xb[fv], lo);
+            if (ALL || (2 * cy >= fylo && 2 * cy < fyhi)) xb[fv] = __dadd_rn(xb[fv], lo);
             if (cy + 1 < nc1) {
                 const double *qn = cc + (int64_t)(cy + 1) * nc1 + hx;
                 const double a_hi = __ldg(qn), b_hi = ox ? __ldg(qn + 1) : 0.0;
@@ -417,7 +418,7 @@ __global__ void __launch_bounds__(kTX *kTY)
                 // (ox=1) diagonal edge (hx,cy)-(hx+1,cy+1)
                 const double mid = ox ? __dadd_rn(__dmul_rn(0.5, a_lo), __dmul_rn(0.5, b_hi))
                                       : __dadd_rn(__dmul_rn(0.5, a_lo), __dmul_rn(0.5, a_hi));
-                if (2 * cy + 1 >= fylo && 2 * cy + 1 < fyhi)
+                if (ALL || (2 * cy + 1 >= fylo && 2 * cy + 1 < fyhi))
                     xb[fv + nf1] = __dadd_rn(xb[fv + nf1], mid);
                 lo = ox ? __dadd_rn(__dmul_rn(0.5, a_hi), __dmul_rn(0.5, b_hi))
                         : __dmul_rn(1.0, a_hi);
