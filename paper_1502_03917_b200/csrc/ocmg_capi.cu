@@ -970,7 +970,7 @@ int ocmg_ne_gs_sweep_strip(const ocmg_level *lv, int forward, int y_begin,
         P.base = pl.base;
         P.rem = pl.rem;
         P.forward = forward ? 1 : 0;
-        P.y_begin = y_begin;
+            P.y_begin = y_begin;
         P.y_end = y_end;
         P.fs_in = P.fs_out = P.fs_x = (int64_t)(slab_end - slab_begin) * n1;
         std::copy(lv->mc_ci, lv->mc_ci + 58, &P.ci[0][0]);

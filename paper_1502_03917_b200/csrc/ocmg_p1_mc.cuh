@@ -137,11 +137,6 @@ __global__ void __launch_bounds__(mcs::NT, 1)
     const int mg = 2 * (13 - q) + 1;  // margin whose result reaches the tile
     const int cxl = max(xl, X0 - mg), cxr = min(xr, X1 + mg);
     const int cyl = max(Ylo, Y0 - mg), cyh = min(Yhi, Y1 + mg);
-    // interior-class coefficients in shared memory (broadcast reads; 14 warps
-    // at <= 128 registers leave no room for them in registers)
-    __shared__ __align__(16) double sci[2][30];
-    if (tid < 58) sci[tid / 29][tid % 29] = P.ci[tid / 29][tid % 29];
-    const double *scw = sci[field], *sca = sci[field] + 14;
     // this lane's vertex at step s: row y = Ylo + s - 3q, column
     // x = xl + o + 7 lane with o = (cm - xl - 2y) mod 7, so o(y+1) = o(y) - 2
     int y = Ylo - 3 * q;
@@ -196,7 +191,10 @@ __global__ void __launch_bounds__(mcs::NT, 1)
             double2 *const adr[7] = {rb - 1, rb, rc - 1, rc, rc + 1, ru, ru + 1};
             double p;
             if (y >= 3 && y <= n1 - 4 && x >= 3 && x <= n1 - 4) {
-                p = node_update<true>(adr, scw, sca, sca[14], nullptr);
+                // coefficients straight from the parameter bank (indexed
+                // LDC: the constant cache, not the shared-memory pipe)
+                p = node_update<true>(adr, P.ci[field], P.ci[field] + 14,
+                                      P.ci[field][28], nullptr);
             } else {
                 const int cls = 7 * p1_axis_class(y, n1) + p1_axis_class(x, n1);
                 p = node_update<false>(adr, nullptr, nullptr, 0.0,
