@@ -635,13 +635,12 @@ __device__ __noinline__ void wf_stage_apply_fast(const WfCtx *C, int j, int FP,
     }
     wfd::cp_async_wait_all();
     __syncwarp();
+    // stencil coefficients read from shared memory at each use (broadcast):
+    // held in registers they pushed this stage over the 96-register cap of a
+    // 19-warp CTA and it spilled
     const double *a = C->sAW + kMidClass * 28 + FP * 7;
-    double A0[7], A1[7];
-#pragma unroll
-    for (int d = 0; d < 7; ++d) {
-        A0[d] = -a[BWD ? 6 - d : d];
-        A1[d] = -a[14 + (BWD ? 6 - d : d)];
-    }
+    auto A0 = [&](int d) { return -a[BWD ? 6 - d : d]; };
+    auto A1 = [&](int d) { return -a[14 + (BWD ? 6 - d : d)]; };
 #pragma unroll
     for (int t = 1; t <= HR; ++t) {
         const int i = rlo - 1 + t;
@@ -657,15 +656,15 @@ __device__ __noinline__ void wf_stage_apply_fast(const WfCtx *C, int j, int FP,
             const int64_t lin = lin0 + (t - 1) * lstep;
 #pragma unroll
             for (int f = 0; f < 2; ++f) {
-                const double *Af = f ? A1 : A0;
+                auto Af = [&](int d) { return f ? A1(d) : A0(d); };
                 double w = bv[t - 1][f];
-                w = fma(Af[0], lp, w);
-                w = fma(Af[1], pv[t - 1], w);
-                w = fma(Af[2], lc, w);
-                w = fma(Af[3], pv[t], w);
-                w = fma(Af[4], rc, w);
-                w = fma(Af[5], pv[t + 1], w);
-                w = fma(Af[6], rn, w);
+                w = fma(Af(0), lp, w);
+                w = fma(Af(1), pv[t - 1], w);
+                w = fma(Af(2), lc, w);
+                w = fma(Af(3), pv[t], w);
+                w = fma(Af(4), rc, w);
+                w = fma(Af(5), pv[t + 1], w);
+                w = fma(Af(6), rn, w);
                 if (okind == 0)
                     C->P.ringu[(int64_t)C->b * C->psu + (int64_t)f * ROWS * RW +
                                (int64_t)i * RW + slot] = w;
