@@ -234,6 +234,9 @@ def kernel_table(dsys, coarse_sys, transfer, x, r, f, stream, iters, hbm):
         time_events(lambda: gs.sweep(x, r), iters, stream), n)
     add("ne_gs_multicolour", "ne_gs",
         time_events(lambda: mc.sweep(x, r), iters, stream), n)
+    cg = P.make_smoother(dsys, "cgs", gs_mode="multicolour")
+    add("cgs_multicolour", "ne_gs",
+        time_events(lambda: cg.sweep(x, r), iters, stream), n)
     add("restrict", "restrict", time_events(
         lambda: transfer.restrict(r, rc), iters, stream), n)
     add("prolong_add", "prolong", time_events(
@@ -249,7 +252,7 @@ def solve_timing(level, alpha, cycle, coarsest, mode, sine, problem="poisson",
     import paper_1502_03917_b200 as P
     t_setup = time.perf_counter()
     kind = (P.SmootherKind("normal", tau=0.4) if smoother == "normal"
-            else P.SmootherKind(smoother))
+            else P.SmootherKind(smoother))  # lsgs / cgs
     cfg = P.CycleConfig(smoother=kind, cycle=cycle,
                         coarsest_level=coarsest, gs_mode=mode)
     mg = P.build_solver(problem, level, alpha, cfg)
@@ -263,7 +266,8 @@ def solve_timing(level, alpha, cycle, coarsest, mode, sine, problem="poisson",
     _, hist = mg.solve_to_tolerance(f, tol=1e-8, max_cycles=300)
     torch.cuda.synchronize()
     t = time.perf_counter() - t0
-    sm_name = "NE-Jacobi(tau=0.4)" if smoother == "normal" else f"NE-GS[{mode}]"
+    sm_name = ("NE-Jacobi(tau=0.4)" if smoother == "normal"
+               else f"CGS[{mode}]" if smoother == "cgs" else f"NE-GS[{mode}]")
     return {"config": f"{problem} L{level} alpha={alpha} {cycle.upper()}(2,2) "
                       f"{sm_name} coarsest L{coarsest}"
                       + (" y_D=U+sin*sin" if sine else ""),
@@ -509,6 +513,10 @@ def run_gpu_arm(args, ws, rank, local):
                                     for m in ("wavefront", "multicolour")]
                 result["solve"].append(solve_timing(10, a, "v", 2, "wavefront",
                                                     False, smoother="normal"))
+            # CGS collective smoother, config-2 shape
+            result["solve"] += [solve_timing(10, 1e-4, "v", 2, m, False,
+                                             smoother="cgs")
+                                for m in ("reference", "multicolour")]
             # Stokes control (configs 4 and 5; generic CSR kernels)
             result["solve"] += [solve_timing(5, 1e-4, "v", 1, m, False, "stokes")
                                 for m in ("wavefront", "multicolour")]

@@ -47,6 +47,7 @@ extern "C" {
 #define OCMG_SMOOTHER_NORMAL 0 /* NE-Jacobi  (reference "normal") */
 #define OCMG_SMOOTHER_LSGS 1   /* NE-GS      (reference "lsgs")   */
 #define OCMG_SMOOTHER_SLSGS 2  /* fwd + bwd NE-GS ("slsgs")        */
+#define OCMG_SMOOTHER_CGS 3    /* collective GS over vertex pairs ("cgs") */
 
 /* NE-GS execution modes */
 #define OCMG_GS_REFERENCE 0   /* level-scheduled, reference arithmetic (bitwise) */
@@ -81,6 +82,12 @@ int ocmg_level_create_csr(int problem, int64_t n, const int64_t *row_off,
                           const double *norm_diag, int n_fields,
                           const int64_t *field_off, uint32_t pressure_mask,
                           int want_colouring, ocmg_level **out);
+
+/* The control weight alpha of a generic (CSR) Poisson level: the collective
+ * smoother's 2x2 solve divides by it (kernels.py:85-88), and it cannot be
+ * recovered bitwise from the assembled -M/alpha block.  Structured levels
+ * get it at creation. */
+int ocmg_level_set_alpha(ocmg_level *lv, double alpha);
 
 /* Structured P1 level (Poisson control, mesh level k >= 3): the operator is
  * held as position-class stencil tables (49 classes x 2 blocks x 7
@@ -149,6 +156,15 @@ int ocmg_restrict_rows(const ocmg_transfer *t, const double *rf, double *rc,
                        int cy_begin, int cy_end, void *stream);
 int ocmg_prolong_add_rows(const ocmg_transfer *t, const double *c, double *xf,
                           int fy_begin, int fy_end, void *stream);
+
+/* One collective Gauss-Seidel sweep over state/adjoint vertex pairs
+ * (kernels.collective_sweep, kernels.py:70-96, via cgs_sweep,
+ * smoothers.py:288-295; Poisson control only): mode OCMG_GS_REFERENCE or
+ * OCMG_GS_WAVEFRONT = the reference's vertex order (bit-identical),
+ * OCMG_GS_MULTICOLOUR = 3-colour order (its own smoother).  scratch: n
+ * doubles.  *ops: touched entries (nnz). */
+int ocmg_cgs_sweep(const ocmg_level *lv, int mode, double *x, double *r,
+                   double *scratch, void *stream, int64_t *ops);
 
 /* Constant-mode removal of the pressure fields (pressure_mean_projection,
  * assembly.py:381-388); no-op for Poisson. */

@@ -59,6 +59,8 @@ def lib():
         L.orc_lsgs_sweep.argtypes = [i64, p, p, p, p, p, p, p, p, p,
                                      ctypes.c_int]
         L.orc_lsgs_sweep.restype = i64
+        L.orc_collective_sweep.argtypes = [i64, p, p, p, p, p, dbl, p, p]
+        L.orc_collective_sweep.restype = i64
         _LIB = L
     return _LIB
 
@@ -555,8 +557,10 @@ class OracleSmoother:
     column weight, normal-equation diagonal (smoothers.py:189-216)."""
 
     def __init__(self, system: OracleSystem, name="lsgs", tau=None):
-        if name not in ("normal", "lsgs", "slsgs"):
+        if name not in ("normal", "lsgs", "slsgs", "cgs"):
             raise ValueError(f"oracle smoother '{name}' not in scope")
+        if name == "cgs" and system.problem != "poisson":
+            raise ValueError("collective sweep needs a scalar control system")
         A = system.A
         self.system, self.name = system, name
         self.tau = tau if tau is not None else DEFAULT_TAU[system.problem]
@@ -576,6 +580,10 @@ class OracleSmoother:
         self.weight = system.L
         self._update = np.empty(system.n)
         self.op_count = 0
+        if name == "cgs":  # smoothers.py:217-219: diag(M), diag(K)
+            nn = system.n // 2
+            self.mass_diag = np.ascontiguousarray(A[:nn, :nn].diagonal())
+            self.stiff_diag = np.ascontiguousarray(A[:nn, nn:].diagonal())
 
     def _args(self):
         return (self.system.n, _ptr(self.row_off), _ptr(self.row_col),
@@ -594,8 +602,18 @@ class OracleSmoother:
             1 if forward else 0)
         return x, r
 
+    def cgs(self, x, r):
+        """kernels.collective_sweep via smoothers.py:288-295."""
+        self.op_count += lib().orc_collective_sweep(
+            self.system.n // 2, _ptr(self.col_off), _ptr(self.col_row),
+            _ptr(self.col_val), _ptr(self.mass_diag), _ptr(self.stiff_diag),
+            float(self.system.alpha), _ptr(x), _ptr(r))
+        return x, r
+
     def sweep(self, x, r):
-        """smoothers.py:226-244 for the NE family."""
+        """smoothers.py:226-244 for the NE family and CGS."""
+        if self.name == "cgs":
+            return self.cgs(x, r)
         if self.name == "normal":
             return self.normal(x, r)
         if self.name == "lsgs":

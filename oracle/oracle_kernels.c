@@ -15,6 +15,7 @@
  *                       y_i = sum over the row, from 0.0, in column order)
  *   orc_normal_sweep <- kernels.py:17-39 (two-phase NE-Jacobi sweep)
  *   orc_lsgs_sweep   <- kernels.py:43-66 (sequential NE-GS sweep)
+ *   orc_collective_sweep <- kernels.py:70-96 (CGS over vertex pairs)
  *
  * All indices int64, values fp64, arrays in the reference's CSR / CSC
  * layout.  Each sweep returns the number of touched matrix entries, as the
@@ -96,6 +97,38 @@ int64_t orc_lsgs_sweep(int64_t n,
         for (int64_t t = col_off[i]; t < col_off[i + 1]; ++t)
             r[col_row[t]] -= col_val[t] * p;
         ops += (row_off[i + 1] - row_off[i]) + (col_off[i + 1] - col_off[i]);
+    }
+    return ops;
+}
+
+/* Collective Gauss-Seidel over state/adjoint vertex pairs (kernels.py:70-96,
+ * smoothers.py:288-295): vertex i owns unknowns (i, i + n_nodes); the local
+ * 2x2 system [[m, k], [k, -m/alpha]] is solved in closed form with the
+ * reference's operation order (no contraction), then both columns are
+ * scattered into r in CSC order. */
+int64_t orc_collective_sweep(int64_t n_nodes,
+                             const int64_t *col_off, const int64_t *col_row,
+                             const double *col_val,
+                             const double *mass_diag, const double *stiff_diag,
+                             double alpha, double *x, double *r)
+{
+    int64_t ops = 0;
+    for (int64_t i = 0; i < n_nodes; ++i) {
+        const int64_t j = i + n_nodes;
+        const double m = mass_diag[i];
+        const double k = stiff_diag[i];
+        const double det = -m * m / alpha - k * k;
+        const double ra = r[i];
+        const double rb = r[j];
+        const double s = (-m / alpha * ra - k * rb) / det;
+        const double t = (-k * ra + m * rb) / det;
+        x[i] += s;
+        x[j] += t;
+        for (int64_t tt = col_off[i]; tt < col_off[i + 1]; ++tt)
+            r[col_row[tt]] -= col_val[tt] * s;
+        for (int64_t tt = col_off[j]; tt < col_off[j + 1]; ++tt)
+            r[col_row[tt]] -= col_val[tt] * t;
+        ops += (col_off[i + 1] - col_off[i]) + (col_off[j + 1] - col_off[j]);
     }
     return ops;
 }

@@ -15,7 +15,7 @@ from .assembly import (BlockSystem, FieldLayout, assemble_p1,
 from .mesh import StructuredMesh
 from .multigrid import (CoarseSolver, CycleConfig, Multigrid, SolveReport,
                         assemble_hierarchy, baseline_rhs, build_solver)
-from .smoothers import (SmootherKind, SmootherState, lsgs_sweep,
+from .smoothers import (SmootherKind, SmootherState, cgs_sweep, lsgs_sweep,
                         make_smoother, normal_equation_sweep, slsgs_sweep)
 from .transfer import (TransferPair, p1_prolongation, p2_prolongation,
                        system_transfer)
@@ -27,7 +27,8 @@ __all__ = [
     "SingularMatrixError", "SmootherKind", "SmootherState", "SolveReport",
     "StructuredMesh", "TransferPair", "assemble_hierarchy", "assemble_p1",
     "assemble_taylor_hood", "baseline_rhs", "build", "build_poisson_system",
-    "build_solver", "build_stokes_system", "lsgs_sweep", "make_smoother",
+    "build_solver", "build_stokes_system", "cgs_sweep", "lsgs_sweep",
+    "make_smoother",
     "normal_equation_sweep", "p1_class_tables", "p1_prolongation",
     "p2_prolongation", "pressure_mean_projection", "slsgs_sweep",
     "system_transfer",

@@ -427,6 +427,8 @@ def build_poisson_system(level, alpha):
                            structured=True, mesh=mesh)
     a, L, mass = _poisson_csr(mesh, alpha)
     h = _create_csr_level(_lib.POISSON, a, L, layout, 0)
+    # the control weight itself (the CGS 2x2 solve divides by it)
+    _lib.call("ocmg_level_set_alpha", h.ptr, float(alpha))
     return BlockSystem(problem="poisson", level=level, alpha=alpha,
                        layout=layout, handle=h, structured=False, mesh=mesh,
                        matrix=a, norm_diag=L, mass=mass)

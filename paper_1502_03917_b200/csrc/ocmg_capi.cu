@@ -16,6 +16,7 @@
 #include "ocmg_p1_mc.cuh"
 #include "ocmg_p1_mc_small.cuh"
 #include "ocmg_subcycle.cuh"
+#include "ocmg_cgs.cuh"
 #include "ocmg_wavefront.cuh"
 
 using namespace ocmg;
@@ -374,6 +375,41 @@ void level_ne_gs(const ocmg_level *lv, int mode, bool forward, double *x,
     }
 }
 
+// one CGS sweep (kernels.py:70-96): mode OCMG_GS_MULTICOLOUR = 3 colours,
+// otherwise the reference order (anti-diagonal levels); scratch: n doubles
+void level_cgs(const ocmg_level *lv, int mode, double *x, double *r, double *scratch,
+               cudaStream_t s) {
+    OCMG_REQUIRE(lv->problem == OCMG_POISSON,
+                 "collective sweep needs a scalar control system");
+    OCMG_REQUIRE(lv->alpha > 0.0, "level has no control weight (ocmg_level_set_alpha)");
+    if (lv->kind != kP1) {
+        OCMG_LAUNCH(k_csr_cgs_seq, 1, 32, 0, s, lv->n / 2, lv->A.off.p, lv->A.col.p,
+                    lv->A.val.p, lv->alpha, x, r);
+        OCMG_LAUNCH_CHECK();
+        return;
+    }
+    const int n1 = lv->n1;
+    const int64_t N = (int64_t)n1 * n1;
+    if (mode == OCMG_GS_MULTICOLOUR) {
+        const int64_t per = (int64_t)((n1 + 2) / 3) * n1;
+        for (int c = 0; c < 3; ++c) {
+            OCMG_LAUNCH(k_p1_cgs_solve, grid_for(per, kBlk), kBlk, 0, s, n1, lv->tables.p,
+                        lv->alpha, 3, c, x, r, scratch);
+            OCMG_LAUNCH(k_p1_cgs_apply, grid_for(N, kBlk), kBlk, 0, s, n1, lv->tables.p,
+                        3, c, scratch, r);
+        }
+    } else {
+        const int blk = n1 < 256 ? 32 * ((n1 + 31) / 32) : 256;
+        for (int l = 0; l <= 2 * (n1 - 1); ++l) {
+            OCMG_LAUNCH(k_p1_cgs_solve, grid_for(n1, blk), blk, 0, s, n1, lv->tables.p,
+                        lv->alpha, 0, l, x, r, scratch);
+            OCMG_LAUNCH(k_p1_cgs_apply, grid_for(5 * (int64_t)n1, kBlk), kBlk, 0, s, n1,
+                        lv->tables.p, 0, l, scratch, r);
+        }
+    }
+    OCMG_LAUNCH_CHECK();
+}
+
 void level_mean_project(const ocmg_level *lv, double *x, cudaStream_t s) {
     if (lv->problem != OCMG_STOKES) return;
     const int nf = (int)lv->field_off.size() - 1;
@@ -605,6 +641,9 @@ void smooth(ocmg_hierarchy *h, int hi, double *x, double *r, cudaStream_t s) {
     case OCMG_SMOOTHER_LSGS:
         level_ne_gs(lv, c.gs_mode, true, x, r, s);
         break;
+    case OCMG_SMOOTHER_CGS:
+        level_cgs(lv, c.gs_mode, x, r, h->scratch[hi].p, s);
+        break;
     default:
         level_ne_gs(lv, c.gs_mode, true, x, r, s);
         level_ne_gs(lv, c.gs_mode, false, x, r, s);
@@ -618,7 +657,7 @@ void smooth_n(ocmg_hierarchy *h, int hi, int nu, double *x, double *r,
     ocmg_level *lv = h->levels[hi - 1];
     const ocmg_cycle_config &c = h->cfg;
     if (!(lv->kind == kP1 && c.gs_mode == OCMG_GS_MULTICOLOUR &&
-          c.smoother != OCMG_SMOOTHER_NORMAL)) {
+          (c.smoother == OCMG_SMOOTHER_LSGS || c.smoother == OCMG_SMOOTHER_SLSGS))) {
         for (int i = 0; i < nu; ++i) smooth(h, hi, x, r, s);
         return;
     }
@@ -675,7 +714,9 @@ void cycle_rec(ocmg_hierarchy *h, int hi, double *x, const double *rhs,
 void setup_subcycle(ocmg_hierarchy *h) {
     h->sub_hi = 0;
     const ocmg_cycle_config &c = h->cfg;
-    if (c.gs_mode != OCMG_GS_MULTICOLOUR || c.smoother == OCMG_SMOOTHER_NORMAL) return;
+    if (c.gs_mode != OCMG_GS_MULTICOLOUR ||
+        !(c.smoother == OCMG_SMOOTHER_LSGS || c.smoother == OCMG_SMOOTHER_SLSGS))
+        return;
     if (!h->coarse->inv.p || h->coarse->problem != OCMG_POISSON) return;
     const ocmg_level *l0 = h->levels[0];
     if (l0->kind != kP1 || l0->k - 1 < 3) return;
@@ -892,6 +933,14 @@ int ocmg_level_create_p1(int k, double alpha, const double *tables,
     });
 }
 
+int ocmg_level_set_alpha(ocmg_level *lv, double alpha) {
+    return guarded([&] {
+        OCMG_REQUIRE(lv, "null level");
+        OCMG_REQUIRE(alpha > 0.0, "alpha must be positive");
+        lv->alpha = alpha;
+    });
+}
+
 int ocmg_level_destroy(ocmg_level *lv) {
     return guarded([&] { delete lv; });
 }
@@ -1012,6 +1061,17 @@ int ocmg_prolong_add_rows(const ocmg_transfer *t, const double *c, double *xf,
         OCMG_REQUIRE(0 <= fy_begin && fy_begin <= fy_end && fy_end <= 2 * t->nc1 - 1,
                      "bad rows");
         do_prolong_add(t, c, xf, as_stream(stream), fy_begin, fy_end);
+    });
+}
+
+int ocmg_cgs_sweep(const ocmg_level *lv, int mode, double *x, double *r,
+                   double *scratch, void *stream, int64_t *ops) {
+    return guarded([&] {
+        OCMG_REQUIRE(lv && x && r && scratch, "null argument");
+        OCMG_REQUIRE(mode >= OCMG_GS_REFERENCE && mode <= OCMG_GS_MULTICOLOUR,
+                     "unknown sweep mode");
+        level_cgs(lv, mode, x, r, scratch, as_stream(stream));
+        if (ops) *ops = lv->nnz;
     });
 }
 
@@ -1156,6 +1216,12 @@ int ocmg_hierarchy_create(int n_levels, ocmg_level *const *levels,
         OCMG_REQUIRE(out && levels && transfers && coarse && cfg,
                      "null argument");
         OCMG_REQUIRE(n_levels >= 1, "need at least one smoothed level");
+        OCMG_REQUIRE(cfg->smoother >= OCMG_SMOOTHER_NORMAL &&
+                         cfg->smoother <= OCMG_SMOOTHER_CGS,
+                     "unknown smoother kind");
+        OCMG_REQUIRE(cfg->smoother != OCMG_SMOOTHER_CGS ||
+                         levels[n_levels - 1]->problem == OCMG_POISSON,
+                     "collective sweep needs a scalar control system");
         OCMG_REQUIRE(cfg->nu_pre + cfg->nu_post >= 1,
                      "need at least one smoothing step per cycle");
         auto h = std::make_unique<ocmg_hierarchy>();
@@ -1178,7 +1244,7 @@ int ocmg_hierarchy_create(int n_levels, ocmg_level *const *levels,
         for (int hi = 1; hi <= n_levels; ++hi) {
             h->r[hi].alloc(sizes[hi]);
             // NE-Jacobi update vector / multicolour ping-pong residual
-            if (cfg->smoother == OCMG_SMOOTHER_NORMAL ||
+            if (cfg->smoother == OCMG_SMOOTHER_NORMAL || cfg->smoother == OCMG_SMOOTHER_CGS ||
                 cfg->gs_mode == OCMG_GS_MULTICOLOUR)
                 h->scratch[hi].alloc(sizes[hi]);
         }

@@ -24,7 +24,7 @@ from . import _lib
 from ._vec import as_device, back_inplace, zeros
 
 SMOOTHER_NAMES = ("normal", "lsgs", "slsgs", "cgs", "vanka")
-DEVICE_SMOOTHERS = ("normal", "lsgs", "slsgs")
+DEVICE_SMOOTHERS = ("normal", "lsgs", "slsgs", "cgs")
 GS_MODES = tuple(_lib.GS_MODES)
 
 # damping defaults of the experiment protocol (smoothers.py:25-29)
@@ -66,7 +66,7 @@ def check_applicability(kind, problem):
     if kind.name not in DEVICE_SMOOTHERS:
         raise NotImplementedError(
             f"smoother '{kind.name}' is outside the B200 hot path "
-            "(normal / lsgs / slsgs only)")
+            "(normal / lsgs / slsgs / cgs only)")
     if kind.name == "normal" and kind.resolved_tau(problem) is None:
         raise ValueError(f"smoother '{kind.name}' needs a damping parameter")
 
@@ -96,6 +96,8 @@ class SmootherState:
         """One smoothing step of the bound kind (smoothers.py:226-244);
         ``post`` only matters for the patch smoother."""
         name = self.kind.name
+        if name == "cgs":
+            return cgs_sweep(self, x, r)
         if name == "normal":
             return normal_equation_sweep(self, x, r)
         if name == "lsgs":
@@ -167,6 +169,23 @@ def lsgs_sweep_into(state, x, r_in, r_out, order="forward"):
               _lib.stream_ptr(), ctypes.byref(ops))
     state.op_count += ops.value
     return x, r_out
+
+
+def cgs_sweep(state, x, r):
+    """Collective Gauss-Seidel over state/adjoint pairs (smoothers.py:288-295
+    -> kernels.py:70-96).  gs_mode "reference"/"wavefront": the reference's
+    vertex order, bit-identical; "multicolour": 3-colour order."""
+    if state.system.problem != "poisson":
+        raise ValueError("collective sweep needs a scalar control system")
+    xd, xnp, rd, rnp = _pair(state, x, r)
+    ops = ctypes.c_int64()
+    _lib.call("ocmg_cgs_sweep", state.system.handle, _lib.GS_MODES[state.gs_mode],
+              _lib.dptr(xd), _lib.dptr(rd), _lib.dptr(state._scratch()),
+              _lib.stream_ptr(), ctypes.byref(ops))
+    state.op_count += ops.value
+    back_inplace(xd, x, xnp)
+    back_inplace(rd, r, rnp)
+    return x, r
 
 
 def slsgs_sweep(state, x, r):

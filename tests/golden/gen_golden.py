@@ -116,6 +116,25 @@ def baseline(problem, k, alpha, smoother, cycle, coarsest, seed, tag,
     print(tag, len(hist), hist[:3], hist[-1])
 
 
+def cgs_sweep_fixture(k, alpha, seed):
+    """CGS collective smoother (kernels.py:70-96, smoothers.py:288-295): one
+    sweep from the same seeded state as sweeps()."""
+    s = ocmg.assemble_hierarchy("poisson", k - 1, k, alpha)[0][-1]
+    rng = np.random.default_rng(seed)
+    x0 = rng.uniform(-1.0, 1.0, s.n)
+    f = rng.uniform(-1.0, 1.0, s.n)
+    r0 = s.residual(x0, f)
+    st = ocmg.make_smoother(s, "cgs")
+    x, r = x0.copy(), r0.copy()
+    st.sweep(x, r)
+    d = {"x0": x0, "f": f, "r0": r0, "cgs_x": x, "cgs_r": r,
+         "cgs_ops": np.array(st.op_count)}
+    x2, r2 = x.copy(), r.copy()
+    st.sweep(x2, r2)
+    d["cgs2_x"], d["cgs2_r"] = x2, r2
+    np.savez_compressed(os.path.join(OUT, f"sweep_poisson_k{k}_cgs.npz"), **d)
+
+
 def reference_protocol(problem, k, alpha, smoother, tag):
     cfg = ocmg.CycleConfig(smoother=ocmg.SmootherKind(smoother))
     mg = ocmg.build_solver(problem, k, alpha, cfg)
@@ -133,6 +152,16 @@ def coarse(problem, alpha):
     np.savez_compressed(os.path.join(OUT, f"coarse_{problem}.npz"),
                         rhs=rhs, x=cs.solve(rhs))
 
+
+if __name__ == "__main__" and sys.argv[1:] == ["cgs"]:
+    # the CGS smoother (added in round 1)
+    ocmg_mesh.MAX_LEVEL = 12
+    cgs_sweep_fixture(4, 1e-6, 11)
+    baseline("poisson", 6, 1e-6, "cgs", "v", 1, 0, "c1_cgs")
+    baseline("poisson", 6, 1e-4, "cgs", "v", 2, 0, "p6_a1e-4_c2_cgs", keep=1)
+    baseline("poisson", 5, 1e-6, "cgs", "w", 1, 0, "p5w_sine_cgs", add_sine=True,
+             keep=1)
+    sys.exit(0)
 
 if __name__ == "__main__":
     ocmg_mesh.MAX_LEVEL = 12

@@ -349,6 +349,11 @@ BASELINE = [
     ("p5w_sine", "poisson", 5, 1e-6, "lsgs", "w", 1, 0, True, "wavefront"),
     ("p6_a1e-4_c2", "poisson", 6, 1e-4, "lsgs", "v", 2, 0, False,
      "wavefront"),
+    # CGS collective smoother, reference vertex order
+    ("c1_cgs", "poisson", 6, 1e-6, "cgs", "v", 1, 0, False, "reference"),
+    ("p6_a1e-4_c2_cgs", "poisson", 6, 1e-4, "cgs", "v", 2, 0, False,
+     "reference"),
+    ("p5w_sine_cgs", "poisson", 5, 1e-6, "cgs", "w", 1, 0, True, "reference"),
 ]
 
 
@@ -377,6 +382,67 @@ def test_baseline_protocol_vs_reference_golden(case, golden):
     assert len(hist) == len(d["hist"])
     assert rel(host(x), d["x_final"]) < 1e-12
     assert rel(np.array(hist), d["hist"]) < 1e-6
+
+
+@pytest.mark.parametrize("k", [2, 4, 6])
+def test_cgs_sweep_bitwise(k, golden):
+    """CGS sweep (kernels.py:70-96) in the reference's vertex order: the
+    anti-diagonal levels (k >= 3) or the sequential CSR kernel (k <= 2) are
+    bit-identical to the oracle; at k = 4 also to the reference's fixture."""
+    osys, dsys = systems("poisson", k, 1e-6)
+    if k == 4:
+        d = golden("sweep_poisson_k4_cgs.npz")
+        x0, r0 = d["x0"], d["r0"]
+    else:
+        x0, _, r0 = inputs(osys, 9)
+    xo, ro = x0.copy(), r0.copy()
+    ost = O.OracleSmoother(osys, "cgs")
+    st = P.make_smoother(dsys, "cgs", gs_mode="reference")
+    xd, rd = dev(x0), dev(r0)
+    for _ in range(2):
+        ost.sweep(xo, ro)
+        st.sweep(xd, rd)
+    assert np.array_equal(host(xd), xo)
+    assert np.array_equal(host(rd), ro)
+    assert st.op_count == ost.op_count
+    if k == 4:
+        x1, r1 = d["x0"].copy(), d["r0"].copy()
+        P.make_smoother(dsys, "cgs", gs_mode="reference").sweep(
+            dev_x := dev(x1), dev_r := dev(r1))
+        assert np.array_equal(host(dev_x), d["cgs_x"])
+        assert np.array_equal(host(dev_r), d["cgs_r"])
+
+
+def test_cgs_multicolour_matches_permuted_oracle():
+    """3-colour CGS = the reference algorithm run in colour order."""
+    k = 5
+    osys, dsys = systems("poisson", k, 1e-6)
+    x0, _, r0 = inputs(osys, 4)
+    n1 = 2 ** k + 1
+    iy, ix = np.divmod(np.arange(n1 * n1), n1)
+    vperm = np.concatenate([np.flatnonzero((ix + iy) % 3 == c) for c in range(3)])
+    perm = np.concatenate([vperm, vperm + n1 * n1])
+    Ap = O.ocmg_oracle._canon(osys.A[perm][:, perm])
+    psys = O.OracleSystem(osys.problem, osys.k, osys.alpha, Ap, osys.L[perm],
+                          osys.fields, osys.mass)
+    xo, ro = x0[perm].copy(), r0[perm].copy()
+    O.OracleSmoother(psys, "cgs").sweep(xo, ro)
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(perm.size)
+    st = P.make_smoother(dsys, "cgs", gs_mode="multicolour")
+    xd, rd = dev(x0), dev(r0)
+    st.sweep(xd, rd)
+    assert rel(host(xd), xo[inv]) < 1e-13
+    assert rel(host(rd), ro[inv]) < 1e-11
+
+
+def test_cgs_multicolour_solve_converges():
+    cfg = P.CycleConfig(smoother=P.SmootherKind("cgs"), cycle="v",
+                        gs_mode="multicolour")
+    mg = P.build_solver("poisson", 7, 1e-6, cfg)
+    f = P.baseline_rhs(mg.finest, 0)
+    _, hist = mg.solve_to_tolerance(f, tol=1e-8, max_cycles=100)
+    assert hist[-1] <= 1e-8 and len(hist) <= 30
 
 
 def test_multicolour_solve_converges():

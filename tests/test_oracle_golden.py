@@ -75,6 +75,20 @@ def test_sweeps(golden, prob, k, alpha):
     assert _rel(r, d["lsgs_bwd_r"]) <= tol
 
 
+def test_cgs_sweep_bitwise(golden):
+    """CGS (kernels.py:70-96) restated in C: bitwise against the reference,
+    one and two sweeps, touched-entry count."""
+    d = golden("sweep_poisson_k4_cgs.npz")
+    s = O.poisson_system(4, 1e-6)
+    st = O.OracleSmoother(s, "cgs")
+    x, r = d["x0"].copy(), d["r0"].copy()
+    st.sweep(x, r)
+    assert np.array_equal(x, d["cgs_x"]) and np.array_equal(r, d["cgs_r"])
+    assert st.op_count == int(d["cgs_ops"])
+    st.sweep(x, r)
+    assert np.array_equal(x, d["cgs2_x"]) and np.array_equal(r, d["cgs2_r"])
+
+
 @pytest.mark.parametrize("prob", ["poisson", "stokes"])
 def test_coarse(golden, prob):
     d = golden(f"coarse_{prob}.npz")
@@ -91,6 +105,10 @@ CASES = [
     ("c1_slsgs", "poisson", 6, 1e-6, "slsgs", "v", 1, 0, False),
     ("c4_lsgs", "stokes", 5, 1e-4, "lsgs", "v", 1, 1, False),
     ("c4_normal", "stokes", 5, 1e-4, "normal", "v", 1, 1, False),
+    # the CGS collective smoother
+    ("c1_cgs", "poisson", 6, 1e-6, "cgs", "v", 1, 0, False),
+    ("p6_a1e-4_c2_cgs", "poisson", 6, 1e-4, "cgs", "v", 2, 0, False),
+    ("p5w_sine_cgs", "poisson", 5, 1e-6, "cgs", "w", 1, 0, True),
     ("p5w_sine", "poisson", 5, 1e-6, "lsgs", "w", 1, 0, True),
     ("p6_a1e-4_c2", "poisson", 6, 1e-4, "lsgs", "v", 2, 0, False),
 ]
