@@ -153,6 +153,28 @@ def coarse(problem, alpha):
                         rhs=rhs, x=cs.solve(rhs))
 
 
+def table_fixture():
+    """cli.run_table on a small sweep."""
+    from ocmg import cli
+    out = {}
+    for prob, levels, smoothers in (("poisson", (3, 5), ("normal", "lsgs", "slsgs", "cgs")),
+                                    ("stokes", (2, 3), ("normal", "lsgs", "slsgs"))):
+        spec = cli.ExperimentSpec(problem=prob, smoothers=smoothers,
+                                  levels=levels, alphas=(1.0, 1e-6))
+        res = cli.run_table(spec)
+        out[prob] = [(c.smoother, c.alpha, c.level, c.iterations, c.converged)
+                     for c in res.cells]
+        print(cli.render_markdown(res))
+    import json
+    with open(os.path.join(OUT, "table_small.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
+
+
+if __name__ == "__main__" and sys.argv[1:] == ["table"]:
+    ocmg_mesh.MAX_LEVEL = 12
+    table_fixture()
+    sys.exit(0)
+
 if __name__ == "__main__" and sys.argv[1:] == ["cgs"]:
     # SURVEY.md §8(f) rank 1: the CGS smoother (added in round 1)
     ocmg_mesh.MAX_LEVEL = 12

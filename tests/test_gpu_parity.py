@@ -445,6 +445,28 @@ def test_cgs_multicolour_solve_converges():
     assert hist[-1] <= 1e-8 and len(hist) <= 30
 
 
+@pytest.mark.parametrize("prob", ["poisson", "stokes"])
+def test_table_runner_matches_reference(prob):
+    """The iteration table (cli.run_table) on the GPU
+    reproduces the reference's own table cell by cell (reference protocol,
+    W-cycle, tol 1e-6, seed 1234; tests/golden/table_small.json)."""
+    import json
+    import os
+
+    from paper_1502_03917_b200 import tables as T
+    want = json.load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                       "table_small.json")))[prob]
+    smoothers = tuple(dict.fromkeys(c[0] for c in want))
+    levels = (min(c[2] for c in want), max(c[2] for c in want))
+    spec = T.ExperimentSpec(problem=prob, smoothers=smoothers, levels=levels,
+                            alphas=(1.0, 1e-6))
+    res = T.run_table(spec)
+    got = [(c.smoother, c.alpha, c.level, c.iterations, c.converged)
+           for c in res.cells]
+    assert got == [tuple(c) for c in want]
+    assert "| level |" in T.render_table(res)
+
+
 def test_multicolour_solve_converges():
     """Multicolour mode is a different smoother: report its own cycle count
     (config-1 shape) and check it converges like NE-GS."""
