@@ -17,6 +17,7 @@
 #include "ocmg_p1_mc_small.cuh"
 #include "ocmg_subcycle.cuh"
 #include "ocmg_cgs.cuh"
+#include "ocmg_cgs_mc.cuh"
 #include "ocmg_wavefront.cuh"
 
 using namespace ocmg;
@@ -73,6 +74,9 @@ struct ocmg_level {
     McsPlan mc;               // one-launch multicolour sweep geometry
     DevBuf<double> mc_r;      // its out-of-place residual
     DevBuf<double> mc_coef;   // [49][2][29] W row, A row, n_diag
+    CgsmPlan cgsm;            // one-launch 3-colour CGS geometry
+    double cgs_mk[49][4] = {};  // per class m, k, -m/alpha, det (CGS 2x2)
+    double cgs_a24[28] = {};    // interior-class A rows
     double mc_ci[58] = {};    // its class-(3,3) rows
     // reduction scratch
     DevBuf<double> partial, scal;
@@ -375,6 +379,9 @@ void level_ne_gs(const ocmg_level *lv, int mode, bool forward, double *x,
     }
 }
 
+// debug: force the six-launch 3-colour CGS form (ocmg__debug_cgs_six_launch)
+bool g_cgs_six_launch = false;
+
 // one CGS sweep (kernels.py:70-96): mode OCMG_GS_MULTICOLOUR = 3 colours,
 // otherwise the reference order (anti-diagonal levels); scratch: n doubles
 void level_cgs(const ocmg_level *lv, int mode, double *x, double *r, double *scratch,
@@ -390,7 +397,24 @@ void level_cgs(const ocmg_level *lv, int mode, double *x, double *r, double *scr
     }
     const int n1 = lv->n1;
     const int64_t N = (int64_t)n1 * n1;
-    if (mode == OCMG_GS_MULTICOLOUR) {
+    if (mode == OCMG_GS_MULTICOLOUR && lv->mc_tier == 2 && !g_cgs_six_launch) {
+        // one launch, residual out of place through the level's mc_r
+        CgsmParams P{};
+        P.n1 = n1;
+        P.nstrips = lv->cgsm.nstrips;
+        P.base = lv->cgsm.base;
+        P.rem = lv->cgsm.rem;
+        P.alpha = lv->alpha;
+        std::copy(&lv->cgs_mk[0][0], &lv->cgs_mk[0][0] + 49 * 4, &P.mk[0][0]);
+        std::copy(lv->cgs_a24, lv->cgs_a24 + 28, P.a24);
+        P.T = lv->tables.p;
+        P.rin = r;
+        P.rout = lv->mc_r.p;
+        P.x = x;
+        OCMG_LAUNCH(k_p1_cgs_mc_sweep, lv->cgsm.grid, cgsm::NT, cgsm::SMEM, s, P);
+        OCMG_CUDA(cudaMemcpyAsync(r, lv->mc_r.p, sizeof(double) * lv->n,
+                                  cudaMemcpyDeviceToDevice, s));
+    } else if (mode == OCMG_GS_MULTICOLOUR) {
         const int64_t per = (int64_t)((n1 + 2) / 3) * n1;
         for (int c = 0; c < 3; ++c) {
             OCMG_LAUNCH(k_p1_cgs_solve, grid_for(per, kBlk), kBlk, 0, s, n1, lv->tables.p,
@@ -914,6 +938,26 @@ int ocmg_level_create_p1(int k, double alpha, const double *tables,
                 OCMG_CUDA(cudaMemset(lv->mc_bar.p, 0, 2 * sizeof(unsigned)));
             }
             if (lv->mc_tier == 2) lv->mc_r.alloc(lv->n);
+            lv->cgsm = cgsm_plan(lv->n1, sms);
+            for (int c = 0; c < 49; ++c) {  // kernels.py:85-88 operation order
+                const double m = tables[kP1OffA + c * 28 + 3];
+                const double k = tables[kP1OffA + c * 28 + 7 + 3];
+                volatile double mm = -m * m;  // no contraction across these
+                volatile double q = mm / alpha;
+                volatile double kk = k * k;
+                lv->cgs_mk[c][0] = m;
+                lv->cgs_mk[c][1] = k;
+                lv->cgs_mk[c][2] = -m / alpha;
+                lv->cgs_mk[c][3] = q - kk;
+            }
+            std::copy(tables + kP1OffA + 24 * 28, tables + kP1OffA + 25 * 28, lv->cgs_a24);
+            static bool attr3 = false;
+            if (!attr3) {
+                OCMG_CUDA(cudaFuncSetAttribute(k_p1_cgs_mc_sweep,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               cgsm::SMEM));
+                attr3 = true;
+            }
             std::vector<double> C(49 * 2 * 29);
             for (int c = 0; c < 49; ++c)
                 for (int f = 0; f < 2; ++f) {
@@ -1418,4 +1462,10 @@ extern "C" int ocmg__debug_subcycle_prof(ocmg_hierarchy *h, double *x, const dou
         OCMG_LAUNCH_CHECK();
         OCMG_CUDA(cudaDeviceSynchronize());
     });
+}
+
+// internal: 1 = multicolour CGS sweeps use the six-launch form on every level
+// (the reference the one-launch kernel must match), 0 = normal dispatch
+extern "C" int ocmg__debug_cgs_six_launch(int on) {
+    return guarded([&] { g_cgs_six_launch = on != 0; });
 }

@@ -436,6 +436,32 @@ def test_cgs_multicolour_matches_permuted_oracle():
     assert rel(host(rd), ro[inv]) < 1e-11
 
 
+@pytest.mark.parametrize("k", [10, 12])
+def test_cgs_one_launch_matches_six_launch(k):
+    """The pipelined one-launch 3-colour CGS sweep is bit-identical to the
+    six-launch (solve + gather per colour) form."""
+    import ctypes
+    dsys = P.build_poisson_system(k, 1e-6)
+    g = torch.Generator(device="cuda").manual_seed(21 + k)
+    x = torch.rand(dsys.n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    r = torch.rand(dsys.n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    x2, r2 = x.clone(), r.clone()
+    st = P.make_smoother(dsys, "cgs", gs_mode="multicolour")
+    fn = _lib.load().ocmg__debug_cgs_six_launch
+    fn.argtypes = [ctypes.c_int]
+    for _ in range(2):
+        st.sweep(x, r)
+    _lib.check(fn(1))
+    try:
+        for _ in range(2):
+            st.sweep(x2, r2)
+    finally:
+        _lib.check(fn(0))
+    torch.cuda.synchronize()
+    assert torch.equal(x, x2)
+    assert torch.equal(r, r2)
+
+
 def test_cgs_multicolour_solve_converges():
     cfg = P.CycleConfig(smoother=P.SmootherKind("cgs"), cycle="v",
                         gs_mode="multicolour")
