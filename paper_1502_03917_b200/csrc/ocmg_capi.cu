@@ -772,13 +772,9 @@ void setup_subcycle(ocmg_hierarchy *h) {
     const SubLayout L = sub_layout(P.nlev, n1s);
     const size_t smem = (size_t)L.total * sizeof(double);
     if (smem > 200 * 1024) return;
-    static bool attr = false;
-    if (!attr) {
-        OCMG_CUDA(cudaFuncSetAttribute(k_p1_subcycle,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       200 * 1024));
-        attr = true;
-    }
+    // per call: the attribute is per device, and cheap to set
+    OCMG_CUDA(cudaFuncSetAttribute(k_p1_subcycle, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   200 * 1024));
     h->sub = P;
     h->sub_smem = smem;
     h->sub_hi = top;
@@ -908,24 +904,16 @@ int ocmg_level_create_p1(int k, double alpha, const double *tables,
         lv->cL[1] = tables[kP1OffL + 24 * 2 + 1];
         lv->wf.init(lv->k, lv->n1, lv->tables.p, lv->tables.p + kP1TableDoubles);
         {
-            static bool attr = false;
-            if (!attr) {
-                OCMG_CUDA(cudaFuncSetAttribute(k_p1_mc_sweep,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               mcs::SMEM));
-                attr = true;
-            }
+            // per call: the attribute is per device, and cheap to set
+            OCMG_CUDA(cudaFuncSetAttribute(k_p1_mc_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           mcs::SMEM));
             int dev = 0, sms = 148;
             OCMG_CUDA(cudaGetDevice(&dev));
             OCMG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
             lv->mc = mcs_plan(lv->n1, sms);
-            static bool attr2 = false;
-            if (!attr2) {
-                OCMG_CUDA(cudaFuncSetAttribute(k_p1_mc_small,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               mc_small_smem(kMcSmallMaxN1)));
-                attr2 = true;
-            }
+            // per call: the attribute is per device, and cheap to set
+            OCMG_CUDA(cudaFuncSetAttribute(k_p1_mc_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           mc_small_smem(kMcSmallMaxN1)));
             lv->mc_tier = lv->n1 <= kMcSmallMaxN1 ? 0 : lv->n1 <= kMcGridMaxN1 ? 1 : 2;
             if (lv->mc_tier == 1) {
                 int occ = 0;
@@ -951,13 +939,9 @@ int ocmg_level_create_p1(int k, double alpha, const double *tables,
                 lv->cgs_mk[c][3] = q - kk;
             }
             std::copy(tables + kP1OffA + 24 * 28, tables + kP1OffA + 25 * 28, lv->cgs_a24);
-            static bool attr3 = false;
-            if (!attr3) {
-                OCMG_CUDA(cudaFuncSetAttribute(k_p1_cgs_mc_sweep,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               cgsm::SMEM));
-                attr3 = true;
-            }
+            // per call: the attribute is per device, and cheap to set
+            OCMG_CUDA(cudaFuncSetAttribute(k_p1_cgs_mc_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           cgsm::SMEM));
             std::vector<double> C(49 * 2 * 29);
             for (int c = 0; c < 49; ++c)
                 for (int f = 0; f < 2; ++f) {
