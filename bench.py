@@ -376,7 +376,7 @@ def run_strip_arm(args, ws, rank, local):
             "config": {"workload": f"poisson_control_L{args.level}_ne_gs_sweep",
                        "unknowns": n, "alpha": args.alpha,
                        "gs_mode": "multicolour",
-                       "step": "ghost exchange (29 rows/side, NCCL P2P) + "
+                       "step": "ghost exchange (15 rows/side, NCCL P2P) + "
                                "one multicolour strip sweep per rank",
                        "l2": "x+r larger than L2 at N<=2; strips of L12 at "
                              "N>=4 may be partly L2-resident",

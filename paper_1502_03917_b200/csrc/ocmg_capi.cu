@@ -1032,10 +1032,10 @@ int ocmg_ne_gs_sweep_strip(const ocmg_level *lv, int forward, int y_begin,
         const int n1 = lv->n1;
         OCMG_REQUIRE(0 <= y_begin && y_begin < y_end && y_end <= n1,
                      "strip rows out of range");
-        OCMG_REQUIRE(slab_begin <= std::max(0, y_begin - 29) &&
-                         slab_end >= std::min(n1, y_end + 29) && slab_begin >= 0 &&
+        OCMG_REQUIRE(slab_begin <= std::max(0, y_begin - (mcs::H + 1)) &&
+                         slab_end >= std::min(n1, y_end + mcs::H + 1) && slab_begin >= 0 &&
                          slab_end <= n1,
-                     "slab must hold 29 ghost rows on each side of the strip");
+                     "slab must hold 15 ghost rows on each side of the strip");
         OCMG_REQUIRE(r_in != r_out, "r_in and r_out must differ");
         int dev = 0, sms = 148;
         OCMG_CUDA(cudaGetDevice(&dev));
@@ -1399,7 +1399,7 @@ extern "C" int ocmg__debug_wf_prof(const ocmg_level *lv, unsigned long long *out
     });
 }
 
-// internal: the multicolour sweep as 14 colour passes (one launch per
+// internal: the multicolour sweep as 7 colour passes (one launch per
 // colour, in place) -- the reference form the one-launch kernel must match
 extern "C" int ocmg__debug_mc_passes(const ocmg_level *lv, int forward, double *x,
                                      double *r, void *stream) {
@@ -1408,10 +1408,10 @@ extern "C" int ocmg__debug_mc_passes(const ocmg_level *lv, int forward, double *
         const int n1 = lv->n1;
         const int64_t work = (int64_t)((n1 + 6) / 7) * n1;
         cudaStream_t s = as_stream(stream);
-        for (int b = 0; b < 14; ++b) {
-            const int c = forward ? b : 13 - b;
+        for (int b = 0; b < kMcColours; ++b) {
+            const int c = forward ? b : kMcColours - 1 - b;
             OCMG_LAUNCH(k_p1_gs_colour, grid_for(work, kBlk), kBlk, 0, s, n1,
-                        lv->tables.p, c, x, r);
+                        lv->tables.p, c, forward ? 1 : 0, x, r);
         }
         OCMG_LAUNCH_CHECK();
     });

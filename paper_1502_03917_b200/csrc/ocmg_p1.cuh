@@ -199,57 +199,73 @@ __global__ void k_p1_gs_level(int n1, const double *__restrict__ T, int t,
     p1_gs_unknown(field, ix, iy, n1, T, x, r);
 }
 
-// One unknown of the multicolour sweep (same formula as mcs::node_update in
-// ocmg_p1_mc.cuh): two FMA chains, times 1/n_diag, r updated by FMA; absent
-// neighbours are skipped (their coefficients are 0 there).
-__device__ __forceinline__ void p1_mc_unknown(int field, int ix, int iy, int n1,
-                                              const double *__restrict__ T,
-                                              double *__restrict__ x,
-                                              double *__restrict__ r) {
+// One vertex of the multicolour sweep (same formula as mcs::node_update in
+// ocmg_p1_mc.cuh): both of its unknowns in turn -- state then adjoint on a
+// forward sweep, adjoint then state on a backward one -- each
+//     p = (sum_d W_d r_S(d) + sum_d W_{7+d} r_A(d)) * (1 / n_diag)
+// (two FMA chains from 0), x += p, r(d) = fma(-A_d, p, r(d)); the second
+// unknown sees the first one's update.  Absent neighbours are skipped (their
+// coefficients are 0).  r goes through L2 only (ld/st.cg): k_p1_mc_grid runs
+// colours back to back in one launch.
+__device__ __forceinline__ void p1_mc_vertex(int ix, int iy, int n1, bool forward,
+                                             const double *__restrict__ T,
+                                             double *__restrict__ x,
+                                             double *__restrict__ r) {
     const int64_t N = (int64_t)n1 * n1;
     const P1Node q = p1_node(ix, iy, n1);
-    const double *W = T + kP1OffW + q.c * 28 + 14 * field;
-    const double *A = T + kP1OffA + q.c * 28 + 14 * field;
-    const double rnd = __drcp_rn(__ldg(T + kP1OffND + q.c * 2 + field));
     double v0[7], v1[7];
 #pragma unroll
     for (int d = 0; d < 7; ++d) {
         v0[d] = q.ex[d] ? __ldcg(r + q.nb[d]) : 0.0;
         v1[d] = q.ex[d] ? __ldcg(r + N + q.nb[d]) : 0.0;
     }
-    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const int field = forward ? u : 1 - u;
+        const double *W = T + kP1OffW + q.c * 28 + 14 * field;
+        const double *A = T + kP1OffA + q.c * 28 + 14 * field;
+        const double rnd = __drcp_rn(__ldg(T + kP1OffND + q.c * 2 + field));
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int d = 0; d < 7; ++d)
+            if (q.ex[d]) {
+                s0 = __fma_rn(__ldg(W + d), v0[d], s0);
+                s1 = __fma_rn(__ldg(W + 7 + d), v1[d], s1);
+            }
+        const double p = __dmul_rn(__dadd_rn(s0, s1), rnd);
+        const int64_t i = field * N + q.v;
+        x[i] = __dadd_rn(x[i], p);
+#pragma unroll
+        for (int d = 0; d < 7; ++d)
+            if (q.ex[d]) {
+                v0[d] = __fma_rn(-__ldg(A + d), p, v0[d]);
+                v1[d] = __fma_rn(-__ldg(A + 7 + d), p, v1[d]);
+            }
+    }
 #pragma unroll
     for (int d = 0; d < 7; ++d)
         if (q.ex[d]) {
-            s0 = __fma_rn(__ldg(W + d), v0[d], s0);
-            s1 = __fma_rn(__ldg(W + 7 + d), v1[d], s1);
-        }
-    const double p = __dmul_rn(__dadd_rn(s0, s1), rnd);
-    const int64_t i = field * N + q.v;
-    x[i] = __dadd_rn(x[i], p);
-#pragma unroll
-    for (int d = 0; d < 7; ++d)
-        if (q.ex[d]) {
-            __stcg(r + q.nb[d], __fma_rn(-__ldg(A + d), p, v0[d]));
-            __stcg(r + N + q.nb[d], __fma_rn(-__ldg(A + 7 + d), p, v1[d]));
+            __stcg(r + q.nb[d], v0[d]);
+            __stcg(r + N + q.nb[d], v1[d]);
         }
 }
 
-// One colour of the distance-2 multicolour order: colour c in 0..13 is
-// field c/7 and (ix + 2 iy) mod 7 == c % 7.  Same-colour unknowns are at
-// graph distance >= 3 (no 19-point offset satisfies dx + 2 dy = 0 mod 7).
+// One colour of the distance-2 multicolour order: colour c in 0..6 is the
+// vertices with (ix + 2 iy) mod 7 == c (graph distance >= 3 between them: no
+// 19-point offset satisfies dx + 2 dy = 0 mod 7), each updating both of its
+// unknowns.  A forward sweep runs colours 0..6, a backward one 6..0.
+constexpr int kMcColours = 7;
 __global__ void k_p1_gs_colour(int n1, const double *__restrict__ T,
-                               int colour, double *__restrict__ x,
+                               int colour, int forward, double *__restrict__ x,
                                double *__restrict__ r) {
     const int per_row = (n1 + 6) / 7;
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= (int64_t)per_row * n1) return;
     const int iy = (int)(k / per_row);
     const int jj = (int)(k - (int64_t)iy * per_row);
-    const int cc = colour % 7;
-    const int ix = ((cc - 2 * iy) % 7 + 7) % 7 + 7 * jj;
+    const int ix = ((colour - 2 * iy) % 7 + 7) % 7 + 7 * jj;
     if (ix >= n1) return;
-    p1_mc_unknown(colour / 7, ix, iy, n1, T, x, r);
+    p1_mc_vertex(ix, iy, n1, forward != 0, T, x, r);
 }
 
 // partial[b] = sum over a grid-strided slice of L_i x_i^2 (both fields)

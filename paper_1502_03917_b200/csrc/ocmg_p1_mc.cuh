@@ -1,77 +1,74 @@
 // Distance-2 multicolour NE-GS sweep on a structured P1 level in ONE launch.
 //
-// Order: colour c in 0..13 is field c/7 and the vertices with
-// (ix + 2 iy) mod 7 == c mod 7; all of colour 0, then all of colour 1, ...
-// (backward: 13 .. 0).  Same-colour unknowns are at graph distance >= 3, so a
-// colour is one parallel step.  Each unknown is the update of kernels.py:57-64
+// Order: colour c in 0..6 is the vertices with (ix + 2 iy) mod 7 == c (graph
+// distance >= 3 between them); colours run 0..6 (backward: 6..0) and every
+// vertex updates both of its unknowns in turn, state then adjoint (backward:
+// adjoint then state).  Each unknown is the update of kernels.py:57-64
 // (p = row_scaled . r / n_diag; x += p; r -= A[:, i] p) in FMA arithmetic
-// (node_update below); the sweep is bit-identical to the 14-pass form
-// (k_p1_gs_colour, ocmg__debug_mc_passes).  The reference-order modes keep the
-// reference's exact arithmetic; this mode is its own smoother.
+// (node_update below, p1_mc_vertex in ocmg_p1.cuh); the sweep is
+// bit-identical to its 7-pass form (k_p1_gs_colour, ocmg__debug_mc_passes).
+// The reference-order modes keep the reference's exact arithmetic; this mode
+// is its own smoother (its own convergence factor).
 //
 // Pipelining.  Colour q of the sweep at row y reads r on rows y-1..y+1 and
 // writes the same rows; colour q+1 at row y' needs colour q finished on rows
 // <= y'+2.  So one CTA streams its rows bottom to top, running colour q on
-// row s - 3q at step s: the 14 colour-rows of a step touch disjoint rows and
+// row s - 3q at step s: the 7 colour-rows of a step touch disjoint rows and
 // are independent, one __syncthreads per step.  Warp q owns colour q, lane m
 // its m-th vertex in the row (vertices of one colour are 7 columns apart).
-// The live rows (s-40 .. s+1) sit in a 44-row shared-memory ring of
-// (state, adjoint) pairs, so every neighbour is one 16-byte access; rows are
-// prefetched PF steps ahead into registers, row s-41 is final and leaves.
+// The live rows (s-19 .. s+1) sit in a 24-row shared-memory ring of
+// (state, adjoint) pairs, so every neighbour is one 16-byte access and a
+// vertex's two unknown updates share one load and one store of its
+// neighbourhood; rows are prefetched PF steps ahead into registers, row
+// s-20 is final and leaves.
 //
 // Decomposition.  A CTA owns W columns x seg_h rows.  The valid region of r
 // shrinks by 2 columns (rows) per colour, so it loads its tile plus a halo of
-// H = 28 on every side, recomputes the halo (only where the result can reach
-// the tile: margin 2(13-q)+1 for colour q) and writes only its own tile.
+// H = 14 on every side, recomputes the halo (only where the result can reach
+// the tile: margin 2(6-q)+1 for colour q) and writes only its own tile.
 // Halos are read from r_in and the tile is written to r_out (out of place:
 // neighbours read what this CTA overwrites); x is updated in place by the
-// owning CTA.  One CTA per SM: strips get base or base+1 row segments so the
-// grid is exactly the SM count.
+// owning CTA.  Two CTAs per SM (79 KB of shared memory each); strips get base
+// or base+1 row segments so the grid fills the SMs once.
 #pragma once
 
 #include "ocmg_p1.cuh"
 
 namespace ocmg {
 namespace mcs {
-constexpr int RING = 44;  // rows s-41 .. s+2
-constexpr int H = 28;     // 2 columns (rows) per colour x 14 colours
-constexpr int NWARP = 14; // one warp per colour of the sweep
+constexpr int NC = kMcColours;     // 7
+constexpr int H = 2 * NC;          // 2 columns (rows) per colour
+constexpr int RING = 3 * (NC - 1) + 6;  // rows s-20 .. s+2 (+1 spare)
+constexpr int NWARP = NC;          // one warp per colour of the sweep
 constexpr int NT = 32 * NWARP;
-constexpr int PF = 4;     // row prefetch depth (steps)
-constexpr int W = 160;    // owned columns per CTA
-constexpr int STRIDE = W + 2 * H + 2;          // + guard column each side
+constexpr int PF = 4;              // row prefetch depth (steps)
+constexpr int W = 176;             // owned columns per CTA
+constexpr int STRIDE = W + 2 * H + 2;  // + guard column each side
 constexpr int SMEM = RING * STRIDE * 16;
-static_assert((W + 2 * H + 6) / 7 <= 32, "one warp per colour-row");
-static_assert(2 * STRIDE <= NT, "one row value per thread");
-static_assert(2 * W <= NT, "one output value per thread");
+constexpr int STORE_LAG = 3 * (NC - 1) + 2;  // row s - STORE_LAG is final at step s
+static_assert((W + 2 * H + 6) / 7 <= 31, "one warp per colour-row, lane 31 free");
+static_assert(2 * STRIDE <= 2 * NT && 2 * W <= 2 * NT, "two values per thread");
 
-// one unknown in the multicolour sweep's arithmetic (mc_unknown in
-// ocmg_p1.cuh is the same formula on global arrays):
+// one unknown (field f of the vertex) in the multicolour sweep's arithmetic:
 //   p = (sum_d W_d r_S(d) + sum_d W_{7+d} r_A(d)) * (1 / n_diag),
 //   each sum an FMA chain from 0; r(d) = fma(-A_d, p, r(d)).
-// Coefficients of absent neighbours are 0 in the tables and the guard cells
-// hold 0, so boundary vertices need no branches, only their class row.
-// cw/ca/rnd: interior class (shared memory), tc: boundary class (global).
-template <bool INTERIOR>
-__device__ __forceinline__ double node_update(double2 *const (&adr)[7],
-                                              const double *cw, const double *ca,
-                                              double rnd,
-                                              const double *__restrict__ tc) {
-    double2 v[7];
-#pragma unroll
-    for (int d = 0; d < 7; ++d) v[d] = *adr[d];
-    auto W = [&](int d) { return INTERIOR ? cw[d] : __ldg(tc + d); };
-    auto A = [&](int d) { return INTERIOR ? ca[d] : __ldg(tc + 14 + d); };
+// v: the neighbourhood (registers), updated in place.  Coefficients of
+// absent neighbours are 0 in the tables and the guard cells hold 0, so
+// boundary vertices need no branches, only their class row.
+// c: W row (14), A row (14), 1/n_diag -- kernel parameters (interior class)
+// or the global table (boundary classes).
+__device__ __forceinline__ double node_update(double2 (&v)[7], const double *c) {
     double s0 = 0.0, s1 = 0.0;
 #pragma unroll
     for (int d = 0; d < 7; ++d) {
-        s0 = __fma_rn(W(d), v[d].x, s0);
-        s1 = __fma_rn(W(7 + d), v[d].y, s1);
+        s0 = __fma_rn(c[d], v[d].x, s0);
+        s1 = __fma_rn(c[7 + d], v[d].y, s1);
     }
-    const double p = __dmul_rn(__dadd_rn(s0, s1), INTERIOR ? rnd : __ldg(tc + 28));
+    const double p = __dmul_rn(__dadd_rn(s0, s1), c[28]);
 #pragma unroll
     for (int d = 0; d < 7; ++d)
-        *adr[d] = make_double2(__fma_rn(-A(d), p, v[d].x), __fma_rn(-A(7 + d), p, v[d].y));
+        v[d] = make_double2(__fma_rn(-c[14 + d], p, v[d].x),
+                            __fma_rn(-c[21 + d], p, v[d].y));
     return p;
 }
 }  // namespace mcs
@@ -83,13 +80,13 @@ struct McsParams {
     double ci[2][29];  // interior class (3,3): W row, A row, 1/n_diag per field
     const double *C;   // [49][2][29]: W row, A row, 1/n_diag per (class, field)
     // addressed by global vertex index y*n1+x (+ field * fs_*): rin must hold
-    // rows [y_begin-29, y_end+29) of the domain, rout and x rows
+    // rows [y_begin-15, y_end+15) of the domain, rout and x rows
     // [y_begin, y_end); a rank passes base pointers shifted by its slab start
     const double *rin;
     double *rout, *x;
 };
 
-__global__ void __launch_bounds__(mcs::NT, 1)
+__global__ void __launch_bounds__(mcs::NT, 2)
     k_p1_mc_sweep(const __grid_constant__ McsParams P) {
     using namespace mcs;
     extern __shared__ double2 ring[];  // [RING][STRIDE] (state, adjoint)
@@ -107,79 +104,112 @@ __global__ void __launch_bounds__(mcs::NT, 1)
     const int xl = max(0, X0 - H), xr = min(n1, X1 + H);
     const int Ylo = max(0, Y0 - H), Yhi = min(n1, Y1 + H);
 
-    // row loader: thread -> (field, local column incl. guards); rows are
-    // fetched while row <= rmax (rows only grow), the rest are zero
-    const int lf = tid / STRIDE, lc = tid - lf * STRIDE;
-    const int lx = xl - 1 + lc;
-    const bool lact = tid < 2 * STRIDE && lx >= xl && lx < xr;
+    // row loader: thread -> two (field, local column incl. guards) entries;
+    // rows are fetched while row <= rmax (rows only grow), the rest are zero
     const int rmax = min(Yhi, n1 - 1);
-    double *ldst = reinterpret_cast<double *>(ring) + 2 * lc + lf;
-    auto slot0 = [&](int y) { return (y - Ylo + 2 * RING) % RING; };
-    if (tid < 2 * STRIDE)
-        for (int y = Ylo - 1; y <= Ylo + 1; ++y)
-            ldst[2 * STRIDE * slot0(y)] =
-                lact && y >= 0 && y <= rmax ? __ldg(P.rin + lf * NI + (int64_t)y * n1 + lx)
-                                            : 0.0;
+    int lx[2], lf[2];
+    bool lact[2];
+    double *ldst[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const int t = tid + e * NT;
+        lf[e] = t >= STRIDE;
+        const int lc = t - lf[e] * STRIDE;
+        lx[e] = xl - 1 + lc;
+        lact[e] = t < 2 * STRIDE && lx[e] >= xl && lx[e] < xr;
+        ldst[e] = t < 2 * STRIDE ? reinterpret_cast<double *>(ring) + 2 * lc + lf[e] : nullptr;
+    }
+    auto slot0 = [&](int y) { return ((y - Ylo) % RING + RING) % RING; };
+    auto fetch = [&](int e, int y) -> double {
+        return lact[e] && y >= 0 && y <= rmax
+                   ? __ldg(P.rin + lf[e] * NI + (int64_t)y * n1 + lx[e])
+                   : 0.0;
+    };
+    for (int y = Ylo - 1; y <= Ylo + 1; ++y)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+            if (ldst[e]) ldst[e][2 * STRIDE * slot0(y)] = fetch(e, y);
     int lrow = Ylo + 2;  // next row to fetch
-    const double *lsrc = P.rin + lf * NI + (int64_t)lrow * n1 + lx;
-    double pf[PF];       // rows s+2 .. s+1+PF in flight
+    double pf[PF][2];    // rows s+2 .. s+1+PF in flight
 #pragma unroll
     for (int i = 0; i < PF; ++i) {
-        pf[i] = lact && lrow <= rmax ? __ldg(lsrc) : 0.0;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) pf[i][e] = fetch(e, lrow);
         ++lrow;
-        lsrc += n1;
     }
     int lslot = slot0(Ylo + 2);  // ring slot of row Ylo+s+2
 
     // compute role: warp q = position q of the sweep
-    const int colour = P.forward ? q : 13 - q;
-    const int field = colour / 7, cm = colour % 7;
-    const int mg = 2 * (13 - q) + 1;  // margin whose result reaches the tile
+    const int colour = P.forward ? q : NC - 1 - q;
+    const int f0 = P.forward ? 0 : 1;  // first field of each vertex
+    const int mg = 2 * (NC - 1 - q) + 1;  // margin whose result reaches the tile
     const int cxl = max(xl, X0 - mg), cxr = min(xr, X1 + mg);
     const int cyl = max(Ylo, Y0 - mg), cyh = min(Yhi, Y1 + mg);
     // this lane's vertex at step s: row y = Ylo + s - 3q, column
-    // x = xl + o + 7 lane with o = (cm - xl - 2y) mod 7, so o(y+1) = o(y) - 2
+    // x = xl + o + 7 lane with o = (colour - xl - 2y) mod 7, so o(y+1) = o(y) - 2
     int y = Ylo - 3 * q;
-    int o = (cm - xl - 2 * y) % 7;
+    int o = (colour - xl - 2 * y) % 7;
     o += o < 0 ? 7 : 0;
     int sy = slot0(y);
-    double *xrow = P.x + field * P.fs_x + (int64_t)y * n1 + xl + 7 * lane;
+    const int64_t FX = P.fs_x;
+    double *xrow = P.x + (int64_t)y * n1 + xl + 7 * lane;
     const int xbase = xl + 7 * lane;
     auto owned = [&](int yy, int xx) {
         return yy >= Y0 && yy < Y1 && xx >= X0 && xx < X1;
     };
-    // x of the vertex two steps ahead (row y+2, o - 4 mod 7)
-    auto xpre = [&]() -> double {
-        const int o2 = o + 3 >= 7 ? o - 4 : o + 3;
-        return owned(y + 2, xbase + o2) ? xrow[2 * (int64_t)n1 + o2] : 0.0;
-    };
-    double xa, xb;
+    // x of the vertex two steps ahead (row y+2, o - 4 mod 7), both fields
+    double xa[2], xb[2];
     {
         const int o1 = o - 2 < 0 ? o + 5 : o - 2;
-        xa = owned(y, xbase + o) ? xrow[o] : 0.0;
-        xb = owned(y + 1, xbase + o1) ? xrow[n1 + o1] : 0.0;
+        const bool w0 = owned(y, xbase + o), w1 = owned(y + 1, xbase + o1);
+#pragma unroll
+        for (int f = 0; f < 2; ++f) {
+            xa[f] = w0 ? xrow[f * FX + o] : 0.0;
+            xb[f] = w1 ? xrow[f * FX + n1 + o1] : 0.0;
+        }
     }
     __syncthreads();
-    // store role: thread -> (field, output column); row Ylo+s-41 leaves at
-    // step s, i.e. steps [s_st0, s_st1)
-    const int sf = tid / W, sx = X0 + (tid - sf * W);
-    const bool sact = tid < 2 * W && sx < X1;
-    const double *ssrc = reinterpret_cast<const double *>(ring) + 2 * (sx - xl + 1) + sf;
-    double *sdst = P.rout + sf * P.fs_out + (int64_t)Y0 * n1 + sx;
-    const int s_st0 = Y0 - Ylo + 41, s_st1 = Y1 - Ylo + 41;
+    // store role: thread -> two (field, output column) entries; row
+    // Ylo+s-STORE_LAG leaves at step s, i.e. steps [s_st0, s_st1)
+    const double *ssrc[2];
+    double *sdst[2];
+    bool sact[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const int t = tid + e * NT;
+        const int sf = t / W, sx = X0 + (t - sf * W);
+        sact[e] = t < 2 * W && sx < X1;
+        ssrc[e] = reinterpret_cast<const double *>(ring) + 2 * (sx - xl + 1) + sf;
+        sdst[e] = P.rout + sf * P.fs_out + (int64_t)Y0 * n1 + sx;
+    }
+    const int s_st0 = Y0 - Ylo + STORE_LAG, s_st1 = Y1 - Ylo + STORE_LAG;
 
-    const int nsteps = (Yhi - Ylo) + 41;
+    const int nsteps = (Yhi - Ylo) + STORE_LAG;
     for (int s = 0; s < nsteps; ++s) {
-        const double lnew = lact && lrow <= rmax ? __ldg(lsrc) : 0.0;
+        double lnew[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) lnew[e] = fetch(e, lrow);
         ++lrow;
-        lsrc += n1;
-        const double xcur = xa;
-        xa = xb;
-        xb = xpre();
-        if (sact && s >= s_st0 && s < s_st1) {
-            const int ss = lslot + 1 == RING ? 0 : lslot + 1;  // slot of row Ylo+s-41
-            *sdst = ssrc[2 * STRIDE * ss];
-            sdst += n1;
+        double xcur[2];
+        {
+            const int o2 = o + 3 >= 7 ? o - 4 : o + 3;
+            const bool w2 = owned(y + 2, xbase + o2);
+#pragma unroll
+            for (int f = 0; f < 2; ++f) {
+                xcur[f] = xa[f];
+                xa[f] = xb[f];
+                xb[f] = w2 ? xrow[f * FX + 2 * (int64_t)n1 + o2] : 0.0;
+            }
+        }
+        if (s >= s_st0 && s < s_st1) {
+            const int ss = lslot + (RING - 2 - STORE_LAG) % RING;  // slot of row Ylo+s-STORE_LAG
+            const int slot = ss >= RING ? ss - RING : ss;
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+                if (sact[e]) {
+                    *sdst[e] = ssrc[e][2 * STRIDE * slot];
+                    sdst[e] += n1;
+                }
         }
         const int x = xbase + o;
         if (y >= cyl && y < cyh && x >= cxl && x < cxr) {
@@ -189,23 +219,37 @@ __global__ void __launch_bounds__(mcs::NT, 1)
             double2 *rb = ring + sb * STRIDE + c0, *rc = ring + sy * STRIDE + c0,
                     *ru = ring + su * STRIDE + c0;
             double2 *const adr[7] = {rb - 1, rb, rc - 1, rc, rc + 1, ru, ru + 1};
-            double p;
+            double2 v[7];
+#pragma unroll
+            for (int d = 0; d < 7; ++d) v[d] = *adr[d];
+            double p[2];
             if (y >= 3 && y <= n1 - 4 && x >= 3 && x <= n1 - 4) {
-                // coefficients straight from the parameter bank (indexed
-                // LDC: the constant cache, not the shared-memory pipe)
-                p = node_update<true>(adr, P.ci[field], P.ci[field] + 14,
-                                      P.ci[field][28], nullptr);
+                // coefficients straight from the parameter bank (indexed LDC:
+                // the constant cache, not the shared-memory pipe)
+                p[f0] = node_update(v, P.ci[f0]);
+                p[1 - f0] = node_update(v, P.ci[1 - f0]);
             } else {
                 const int cls = 7 * p1_axis_class(y, n1) + p1_axis_class(x, n1);
-                p = node_update<false>(adr, nullptr, nullptr, 0.0,
-                                       P.C + (cls * 2 + field) * 29);
+                p[f0] = node_update(v, P.C + (cls * 2 + f0) * 29);
+                p[1 - f0] = node_update(v, P.C + (cls * 2 + 1 - f0) * 29);
             }
-            if (owned(y, x)) xrow[o] = __dadd_rn(xcur, p);
-        }
-        if (tid < 2 * STRIDE) ldst[2 * STRIDE * lslot] = pf[0];
 #pragma unroll
-        for (int i = 0; i + 1 < PF; ++i) pf[i] = pf[i + 1];
-        pf[PF - 1] = lnew;
+            for (int d = 0; d < 7; ++d) *adr[d] = v[d];
+            if (owned(y, x)) {
+                xrow[o] = __dadd_rn(xcur[0], p[0]);
+                xrow[FX + o] = __dadd_rn(xcur[1], p[1]);
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+            if (ldst[e]) ldst[e][2 * STRIDE * lslot] = pf[0][e];
+#pragma unroll
+        for (int i = 0; i + 1 < PF; ++i) {
+            pf[i][0] = pf[i + 1][0];
+            pf[i][1] = pf[i + 1][1];
+        }
+        pf[PF - 1][0] = lnew[0];
+        pf[PF - 1][1] = lnew[1];
         // advance: row y+1
         lslot = lslot + 1 == RING ? 0 : lslot + 1;
         sy = sy + 1 == RING ? 0 : sy + 1;
@@ -217,7 +261,7 @@ __global__ void __launch_bounds__(mcs::NT, 1)
 }
 
 // host-side launch geometry: strips of W columns; base or base+1 row
-// segments per strip so that the grid fills the SMs once
+// segments per strip so that the grid fills the SMs (two CTAs each) once
 struct McsPlan {
     int nstrips = 0, base = 0, rem = 0, grid = 0;
 };
@@ -226,9 +270,9 @@ inline McsPlan mcs_plan(int n1, int sm_count, int rows = -1) {
     McsPlan p;
     if (rows < 0) rows = n1;
     p.nstrips = (n1 + mcs::W - 1) / mcs::W;
-    // segments much shorter than the pipeline fill (2H + 41 rows) waste steps
-    const int max_seg = std::max(1, rows / 32);
-    const int total = std::max(p.nstrips, std::min(sm_count, p.nstrips * max_seg));
+    // segments much shorter than the pipeline fill (2H + STORE_LAG rows) waste steps
+    const int max_seg = std::max(1, rows / 24);
+    const int total = std::max(p.nstrips, std::min(2 * sm_count, p.nstrips * max_seg));
     p.base = total / p.nstrips;
     p.rem = total % p.nstrips;
     p.grid = p.nstrips * (p.base + (p.rem ? 1 : 0));

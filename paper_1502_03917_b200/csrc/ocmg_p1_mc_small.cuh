@@ -1,12 +1,12 @@
 // Multicolour NE-GS sweep for the small and middle levels of a cycle, where
 // the pipelined strip kernel (ocmg_p1_mc.cuh) would spend most of its steps
-// filling and draining.  Same order and arithmetic (p1_mc_unknown /
+// filling and draining.  Same order and arithmetic (p1_mc_vertex /
 // mcs::node_update), so all three forms are bit-identical.
 //
 //   k <= 6  (n1 <= 65):  k_p1_mc_small -- one CTA, the whole residual in
-//                        shared memory (guard ring of zeros), 14 colour
+//                        shared memory (guard ring of zeros), 7 colour
 //                        phases separated by __syncthreads.
-//   7 <= k <= 9:         k_p1_mc_grid -- one cooperative launch, 14 colour
+//   7 <= k <= 9:         k_p1_mc_grid -- one cooperative launch, 7 colour
 //                        phases separated by a grid barrier, in place.
 #pragma once
 
@@ -40,9 +40,9 @@ __global__ void __launch_bounds__(1024)
     __syncthreads();
     const int per_row = (n1 + 6) / 7;
     const int count = per_row * n1;
-    for (int b = 0; b < 14; ++b) {
-        const int colour = forward ? b : 13 - b;
-        const int field = colour / 7, cm = colour % 7;
+    const int f0 = forward ? 0 : 1;
+    for (int b = 0; b < kMcColours; ++b) {
+        const int cm = forward ? b : kMcColours - 1 - b;
         for (int k = threadIdx.x; k < count; k += blockDim.x) {
             const int iy = k / per_row, jj = k - iy * per_row;
             const int ix = ((cm - 2 * iy) % 7 + 7) % 7 + 7 * jj;
@@ -50,11 +50,18 @@ __global__ void __launch_bounds__(1024)
             const int c = (iy + 1) * P + ix + 1;
             double2 *const adr[7] = {g + c - P - 1, g + c - P, g + c - 1, g + c,
                                      g + c + 1,     g + c + P, g + c + P + 1};
+            double2 v[7];
+#pragma unroll
+            for (int d = 0; d < 7; ++d) v[d] = *adr[d];
             const int cls = 7 * p1_axis_class(iy, n1) + p1_axis_class(ix, n1);
-            const double p = mcs::node_update<false>(adr, nullptr, nullptr, 0.0,
-                                                     C + (cls * 2 + field) * 29);
-            const int64_t xi = field * N + (int64_t)iy * n1 + ix;
-            x[xi] = __dadd_rn(x[xi], p);
+            double p[2];
+            p[f0] = mcs::node_update(v, C + (cls * 2 + f0) * 29);
+            p[1 - f0] = mcs::node_update(v, C + (cls * 2 + 1 - f0) * 29);
+#pragma unroll
+            for (int d = 0; d < 7; ++d) *adr[d] = v[d];
+            const int64_t xi = (int64_t)iy * n1 + ix;
+            x[xi] = __dadd_rn(x[xi], p[0]);
+            x[N + xi] = __dadd_rn(x[N + xi], p[1]);
         }
         __syncthreads();
     }
@@ -94,16 +101,15 @@ __global__ void __launch_bounds__(256)
     const int per_row = (n1 + 6) / 7;
     const int64_t count = (int64_t)per_row * n1;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int b = 0; b < 14; ++b) {
-        const int colour = forward ? b : 13 - b;
-        const int cm = colour % 7;
+    for (int b = 0; b < kMcColours; ++b) {
+        const int cm = forward ? b : kMcColours - 1 - b;
         for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < count;
              k += stride) {
             const int iy = (int)(k / per_row), jj = (int)(k - (int64_t)iy * per_row);
             const int ix = ((cm - 2 * iy) % 7 + 7) % 7 + 7 * jj;
-            if (ix < n1) p1_mc_unknown(colour / 7, ix, iy, n1, T, x, r);
+            if (ix < n1) p1_mc_vertex(ix, iy, n1, forward != 0, T, x, r);
         }
-        if (b < 13) mc_grid_barrier(bar, bar + 1, gridDim.x);
+        if (b < kMcColours - 1) mc_grid_barrier(bar, bar + 1, gridDim.x);
     }
 }
 

@@ -107,43 +107,31 @@ __device__ __forceinline__ void residual(int n1, const double *At, const double 
     __syncthreads();
 }
 
-// mcs::node_update<false> with the table in shared memory; neighbours of the
-// padded-grid cell c (row pitch P) addressed directly (no pointer array)
-__device__ __forceinline__ double node_update_sm(double2 *R, int c, int P, const double *tc) {
-    const int off[7] = {-P - 1, -P, -1, 0, 1, P, P + 1};
-    double2 v[7];
-#pragma unroll
-    for (int d = 0; d < 7; ++d) v[d] = R[c + off[d]];
-    double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-    for (int d = 0; d < 7; ++d) {
-        s0 = __fma_rn(tc[d], v[d].x, s0);
-        s1 = __fma_rn(tc[7 + d], v[d].y, s1);
-    }
-    const double p = __dmul_rn(__dadd_rn(s0, s1), tc[28]);
-#pragma unroll
-    for (int d = 0; d < 7; ++d)
-        R[c + off[d]] = make_double2(__fma_rn(-tc[14 + d], p, v[d].x),
-                                     __fma_rn(-tc[21 + d], p, v[d].y));
-    return p;
-}
-
 __device__ __forceinline__ void sweep(int n1, const double *Ct, double *X, double2 *R,
                                       bool forward) {
     const int N = n1 * n1, P = n1 + 2;
     const int per_row = (n1 + 6) / 7, count = per_row * n1;
-    for (int b = 0; b < 14; ++b) {
-        const int colour = forward ? b : 13 - b;
-        const int field = colour / 7, cm = colour % 7;
+    const int f0 = forward ? 0 : 1;
+    for (int b = 0; b < kMcColours; ++b) {
+        const int cm = forward ? b : kMcColours - 1 - b;
         for (int k = threadIdx.x; k < count; k += blockDim.x) {
             const int iy = k / per_row, jj = k - iy * per_row;
             const int ix = ((cm - 2 * iy) % 7 + 7) % 7 + 7 * jj;
             if (ix >= n1) continue;
             const int c = (iy + 1) * P + ix + 1;
+            const int off[7] = {-P - 1, -P, -1, 0, 1, P, P + 1};
+            double2 v[7];
+#pragma unroll
+            for (int d = 0; d < 7; ++d) v[d] = R[c + off[d]];
             const int cls = 7 * p1_axis_class(iy, n1) + p1_axis_class(ix, n1);
-            const double p = node_update_sm(R, c, P, Ct + (cls * 2 + field) * 29);
-            const int xi = field * N + iy * n1 + ix;
-            X[xi] = __dadd_rn(X[xi], p);
+            double p[2];
+            p[f0] = mcs::node_update(v, Ct + (cls * 2 + f0) * 29);
+            p[1 - f0] = mcs::node_update(v, Ct + (cls * 2 + 1 - f0) * 29);
+#pragma unroll
+            for (int d = 0; d < 7; ++d) R[c + off[d]] = v[d];
+            const int xi = iy * n1 + ix;
+            X[xi] = __dadd_rn(X[xi], p[0]);
+            X[N + xi] = __dadd_rn(X[N + xi], p[1]);
         }
         __syncthreads();
     }

@@ -2,9 +2,9 @@
 
 One process per GPU; rank p owns the mesh rows [y0, y1) of a structured P1
 level (all fields of a vertex on the same rank, rows split as evenly as
-possible).  The multicolour NE-GS sweep needs 29 ghost rows of the residual
-on each side: the pipelined kernel recomputes a 28-row halo (2 rows per
-colour x 14 colours) and reads one more row.  One sweep is then
+possible).  The multicolour NE-GS sweep needs 15 ghost rows of the residual
+on each side: the pipelined kernel recomputes a 14-row halo (2 rows per
+colour x 7 vertex colours) and reads one more row.  One sweep is then
 
     exchange_ghosts(r_in)            # one send/recv pair per neighbour
     ocmg_ne_gs_sweep_strip(...)      # the single-GPU kernel on the slab
@@ -25,7 +25,7 @@ import ctypes
 
 from . import _lib
 
-GHOST = 29
+GHOST = 15
 
 
 class StripPartition:
@@ -299,12 +299,12 @@ class _RankState:
 
 class StripMultigrid:
     """The BASELINE V/W cycle with its fine levels split into row strips
-    (SURVEY.md §8(e)).  Levels whose strips would be thinner than the 29
+    (SURVEY.md §8(e)).  Levels whose strips would be thinner than the 15
     ghost rows of a sweep are gathered: every rank runs the same single-GPU
     sub-cycle on them (ocmg_cycle of the hierarchy topped there).
 
     Per partitioned level visit: x ghost (1 row) -> residual rows; per sweep
-    r ghost (29 rows) -> strip sweep (residual ping-pong); r ghost (1 row) ->
+    r ghost (15 rows) -> strip sweep (residual ping-pong); r ghost (1 row) ->
     restriction rows; coarse visit(s); coarse x ghost (1 row) -> prolongation
     rows; residual; post-sweeps.  Every row is computed with the single-GPU
     kernels' arithmetic, so the iterate is bit-identical to Multigrid's.

@@ -150,12 +150,14 @@ def test_wavefront_vs_reference_mode_many_bands(k, order):
 def _colour_perm(osys, dsys):
     """Unknown order of the multicolour sweep."""
     if osys.problem == "poisson":
+        # vertex colours (ix + 2 iy) mod 7 in turn; each vertex's state then
+        # adjoint unknown
         n1 = 2 ** osys.k + 1
         iy, ix = np.divmod(np.arange(n1 * n1), n1)
         col = (ix + 2 * iy) % 7
         N = n1 * n1
-        return np.concatenate([np.flatnonzero(col == c) + b * N
-                               for b in range(2) for c in range(7)])
+        verts = np.concatenate([np.flatnonzero(col == c) for c in range(7)])
+        return np.stack([verts, verts + N], axis=1).reshape(-1)
     # generic levels: greedy distance-2 colouring in index order
     A = osys.A
     colour = -np.ones(osys.n, dtype=np.int64)

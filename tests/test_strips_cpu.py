@@ -14,8 +14,8 @@ from paper_1502_03917_b200.strips import (GHOST, StripPartition,  # noqa: E402
                                           ghost_plan)
 
 
-@pytest.mark.parametrize("n1,ws", [(65, 2), (257, 3), (1025, 8), (4097, 8),
-                                   (4097, 5)])
+@pytest.mark.parametrize("n1,ws", [(65, 2), (65, 4), (257, 3), (1025, 8),
+                                   (4097, 8), (4097, 5)])
 def test_partition_tiles_rows_and_plans_match(n1, ws):
     parts = [StripPartition(n1, ws, p) for p in range(ws)]
     assert parts[0].y0 == 0 and parts[-1].y1 == n1
@@ -36,7 +36,7 @@ def test_partition_tiles_rows_and_plans_match(n1, ws):
 
 def test_partition_rejects_thin_strips():
     with pytest.raises(ValueError):
-        StripPartition(65, 4, 0)
+        StripPartition(33, 4, 0)  # 8-row strips < GHOST
 
 
 def _free_port():
