@@ -71,6 +71,27 @@ __device__ __forceinline__ double node_update(double2 (&v)[7], const double *c) 
                             __fma_rn(-c[21 + d], p, v[d].y));
     return p;
 }
+// the same update with the coefficients read from shared memory by explicit
+// 16-byte ld.shared (asm volatile: one load per use, never hoisted into
+// registers -- the 58 interior coefficients would not fit beside the
+// neighbourhood at 2 CTAs per SM, and indexed LDC from the parameter bank
+// was a fifth of all instructions); cs: shared-memory address of a 30-double
+// row (W 14, A 14, 1/n_diag, pad), 16-byte aligned
+__device__ __forceinline__ double2 lds2(unsigned a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double node_update_s(double2 (&v)[7], unsigned cs) {
+    double c[30];
+#pragma unroll
+    for (int i = 0; i < 15; ++i) {
+        const double2 t = lds2(cs + 16 * i);
+        c[2 * i] = t.x;
+        c[2 * i + 1] = t.y;
+    }
+    return node_update(v, c);
+}
 }  // namespace mcs
 
 struct McsParams {
@@ -129,6 +150,8 @@ __global__ void __launch_bounds__(mcs::NT, 2)
 #pragma unroll
         for (int e = 0; e < 2; ++e)
             if (ldst[e]) ldst[e][2 * STRIDE * slot0(y)] = fetch(e, y);
+    // steady state: one pointer per entry advanced a row per step, and the
+    // rows still to fetch counted down (rows only grow; past rmax: zeros)
     int lrow = Ylo + 2;  // next row to fetch
     double pf[PF][2];    // rows s+2 .. s+1+PF in flight
 #pragma unroll
@@ -137,6 +160,11 @@ __global__ void __launch_bounds__(mcs::NT, 2)
         for (int e = 0; e < 2; ++e) pf[i][e] = fetch(e, lrow);
         ++lrow;
     }
+    const double *lsrc[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+        lsrc[e] = P.rin + lf[e] * NI + (int64_t)lrow * n1 + lx[e];
+    int lleft = lrow <= rmax ? rmax - lrow + 1 : 0;  // valid rows left to fetch
     int lslot = slot0(Ylo + 2);  // ring slot of row Ylo+s+2
 
     // compute role: warp q = position q of the sweep
@@ -145,6 +173,11 @@ __global__ void __launch_bounds__(mcs::NT, 2)
     const int mg = 2 * (NC - 1 - q) + 1;  // margin whose result reaches the tile
     const int cxl = max(xl, X0 - mg), cxr = min(xr, X1 + mg);
     const int cyl = max(Ylo, Y0 - mg), cyh = min(Yhi, Y1 + mg);
+    // interior coefficients in shared memory (see node_update_s)
+    __shared__ __align__(16) double sci[2][30];
+    if (tid < 58) sci[tid / 29][tid % 29] = P.ci[tid / 29][tid % 29];
+    const unsigned sci0 = (unsigned)__cvta_generic_to_shared(&sci[f0][0]);
+    const unsigned sci1 = (unsigned)__cvta_generic_to_shared(&sci[1 - f0][0]);
     // this lane's vertex at step s: row y = Ylo + s - 3q, column
     // x = xl + o + 7 lane with o = (colour - xl - 2y) mod 7, so o(y+1) = o(y) - 2
     int y = Ylo - 3 * q;
@@ -188,8 +221,11 @@ __global__ void __launch_bounds__(mcs::NT, 2)
     for (int s = 0; s < nsteps; ++s) {
         double lnew[2];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) lnew[e] = fetch(e, lrow);
-        ++lrow;
+        for (int e = 0; e < 2; ++e) {
+            lnew[e] = lact[e] && lleft > 0 ? __ldg(lsrc[e]) : 0.0;
+            lsrc[e] += n1;
+        }
+        lleft -= lleft > 0 ? 1 : 0;
         double xcur[2];
         {
             const int o2 = o + 3 >= 7 ? o - 4 : o + 3;
@@ -226,8 +262,8 @@ __global__ void __launch_bounds__(mcs::NT, 2)
             if (y >= 3 && y <= n1 - 4 && x >= 3 && x <= n1 - 4) {
                 // coefficients straight from the parameter bank (indexed LDC:
                 // the constant cache, not the shared-memory pipe)
-                p[f0] = node_update(v, P.ci[f0]);
-                p[1 - f0] = node_update(v, P.ci[1 - f0]);
+                p[f0] = node_update_s(v, sci0);
+                p[1 - f0] = node_update_s(v, sci1);
             } else {
                 const int cls = 7 * p1_axis_class(y, n1) + p1_axis_class(x, n1);
                 p[f0] = node_update(v, P.C + (cls * 2 + f0) * 29);
