@@ -287,7 +287,7 @@ void level_ne_jacobi(const ocmg_level *lv, double tau, double *x, double *r,
 }
 
 void run_schedule(const ocmg_level *lv, const Schedule &S, bool reverse,
-                  double *x, double *r, cudaStream_t s) {
+                  double *x, double *r, cudaStream_t s, bool warp_rows = false) {
     const int64_t nb = (int64_t)S.off.size() - 1;
     if (lv->n <= kCsrSmallN) {
         // small level: every group in one CTA, __syncthreads between groups
@@ -301,10 +301,18 @@ void run_schedule(const ocmg_level *lv, const Schedule &S, bool reverse,
         const int64_t l = reverse ? nb - 1 - b : b;
         const int64_t lo = S.off[l], cnt = S.off[l + 1] - lo;
         if (!cnt) continue;
-        const int blk = cnt < 128 ? 32 * (int)((cnt + 31) / 32) : 128;
-        OCMG_LAUNCH(k_csr_gs_rows, grid_for(cnt, blk), blk, 0, s, 
-            (int)cnt, S.rows.p + lo, lv->A.off.p, lv->A.col.p, lv->A.val.p,
-            lv->W.p, lv->ndiag.p, x, r);
+        if (warp_rows) {
+            const int64_t thr = cnt * 32;
+            const int blk = thr < 256 ? (int)thr : 256;
+            OCMG_LAUNCH(k_csr_gs_rows_warp, grid_for(thr, blk), blk, 0, s, (int)cnt,
+                        S.rows.p + lo, lv->A.off.p, lv->A.col.p, lv->A.val.p, lv->W.p,
+                        lv->ndiag.p, x, r);
+        } else {
+            const int blk = cnt < 128 ? 32 * (int)((cnt + 31) / 32) : 128;
+            OCMG_LAUNCH(k_csr_gs_rows, grid_for(cnt, blk), blk, 0, s, (int)cnt,
+                        S.rows.p + lo, lv->A.off.p, lv->A.col.p, lv->A.val.p, lv->W.p,
+                        lv->ndiag.p, x, r);
+        }
     }
     OCMG_LAUNCH_CHECK();
 }
@@ -375,7 +383,10 @@ void level_ne_gs(const ocmg_level *lv, int mode, bool forward, double *x,
                      "multicolour NE-GS needs a level created with colouring");
         run_schedule(lv, lv->colours, !forward, x, r, s);
     } else {
-        run_schedule(lv, lv->sched[forward ? 0 : 1], false, x, r, s);
+        // wavefront mode: reference order, warp per row (FMA; 1e-12);
+        // reference mode: thread per row, the reference's arithmetic
+        run_schedule(lv, lv->sched[forward ? 0 : 1], false, x, r, s,
+                     mode == OCMG_GS_WAVEFRONT);
     }
 }
 

@@ -148,6 +148,36 @@ __global__ void k_csr_gs_rows(int cnt, const int32_t *__restrict__ rows,
     csr_gs_row(rows[k], off, col, val, w, ndiag, x, r);
 }
 
+// The same row update with one warp per row (the "wavefront" mode on
+// generic levels: reference order, FMA arithmetic and a tree-summed dot
+// product, held to 1e-12 like the structured wavefront sweep): lanes gather
+// the row in parallel, a butterfly sums it, lanes scatter in parallel.  The
+// thread-per-row form serializes a ~38-term chain and the scatter's
+// read-modify-writes (Stokes rows).
+__global__ void k_csr_gs_rows_warp(int cnt, const int32_t *__restrict__ rows,
+                                   const int64_t *__restrict__ off,
+                                   const int32_t *__restrict__ col,
+                                   const double *__restrict__ val,
+                                   const double *__restrict__ w,
+                                   const double *__restrict__ ndiag,
+                                   double *__restrict__ x, double *__restrict__ r) {
+    const int wid = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (wid >= cnt) return;
+    const int32_t i = rows[wid];
+    const int64_t b = off[i], e = off[i + 1];
+    double q = 0.0;
+    for (int64_t t = b + lane; t < e; t += 32) q = fma(w[t], r[col[t]], q);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    const double p = q / ndiag[i];
+    if (lane == 0) x[i] += p;
+    for (int64_t t = b + lane; t < e; t += 32) {
+        const int32_t j = col[t];
+        r[j] = fma(-val[t], p, r[j]);
+    }
+}
+
 // Whole sweep of a small level in one CTA: the groups (dependency levels or
 // colours) in order, __syncthreads between them (one launch instead of one
 // per group -- the coarse levels of a W-cycle are visited thousands of times)
