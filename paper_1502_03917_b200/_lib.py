@@ -12,6 +12,8 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libocmg_b200.so")
+# developer A/B builds (scripts/): load another build of the same CUDA library
+LIB_PATH = os.environ.get("OCMG_LIB", LIB_PATH)
 CSRC = os.path.join(HERE, "csrc")
 
 OCMG_OK = 0

@@ -7,6 +7,7 @@
 // ocmg_wavefront.cuh.
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <memory>
 
 #include "ocmg_common.cuh"
@@ -78,6 +79,7 @@ struct ocmg_level {
     double cgs_mk[49][4] = {};  // per class m, k, -m/alpha, det (CGS 2x2)
     double cgs_a24[28] = {};    // interior-class A rows
     double mc_ci[58] = {};    // its class-(3,3) rows
+    double mc_cu[mcs::NU] = {};  // their distinct values (mcs::umap)
     // reduction scratch
     DevBuf<double> partial, scal;
 };
@@ -346,12 +348,12 @@ bool p1_mc_sweep(const ocmg_level *lv, bool forward, double *x, double *r,
     P.y_begin = 0;
     P.y_end = lv->n1;
     P.fs_in = P.fs_out = P.fs_x = (int64_t)lv->n1 * lv->n1;
-    std::copy(lv->mc_ci, lv->mc_ci + 58, &P.ci[0][0]);
+    std::copy(lv->mc_cu, lv->mc_cu + mcs::NU, P.cu);
     P.C = lv->mc_coef.p;
     P.rin = r;
     P.rout = rout;
     P.x = x;
-    OCMG_LAUNCH(k_p1_mc_sweep, lv->mc.grid, mcs::NT, mcs::SMEM, s, P);
+    mcs_launch(P, lv->mc.grid, s);
     OCMG_LAUNCH_CHECK();
     return true;
 }
@@ -916,8 +918,7 @@ int ocmg_level_create_p1(int k, double alpha, const double *tables,
         lv->wf.init(lv->k, lv->n1, lv->tables.p, lv->tables.p + kP1TableDoubles);
         {
             // per call: the attribute is per device, and cheap to set
-            OCMG_CUDA(cudaFuncSetAttribute(k_p1_mc_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           mcs::SMEM));
+            mcs_set_smem();
             int dev = 0, sms = 148;
             OCMG_CUDA(cudaGetDevice(&dev));
             OCMG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -965,6 +966,8 @@ int ocmg_level_create_p1(int k, double alpha, const double *tables,
                 }
             lv->mc_coef.upload(C.data(), (int64_t)C.size());
             std::copy(C.data() + 24 * 58, C.data() + 25 * 58, lv->mc_ci);
+            OCMG_REQUIRE(mcs_fill_cu(lv->mc_cu, lv->mc_ci),
+                         "interior stencil row lacks the P1 mesh symmetry");
         }
         lv->partial.alloc(kRedGrid);
         lv->scal.alloc(8);
@@ -1061,12 +1064,12 @@ int ocmg_ne_gs_sweep_strip(const ocmg_level *lv, int forward, int y_begin,
             P.y_begin = y_begin;
         P.y_end = y_end;
         P.fs_in = P.fs_out = P.fs_x = (int64_t)(slab_end - slab_begin) * n1;
-        std::copy(lv->mc_ci, lv->mc_ci + 58, &P.ci[0][0]);
+        std::copy(lv->mc_cu, lv->mc_cu + mcs::NU, P.cu);
         P.C = lv->mc_coef.p;
         P.rin = r_in - (int64_t)slab_begin * n1;
         P.rout = r_out - (int64_t)slab_begin * n1;
         P.x = x - (int64_t)slab_begin * n1;
-        OCMG_LAUNCH(k_p1_mc_sweep, pl.grid, mcs::NT, mcs::SMEM, as_stream(stream), P);
+        mcs_launch(P, pl.grid, as_stream(stream));
         OCMG_LAUNCH_CHECK();
         if (ops) *ops = 2 * lv->nnz * (int64_t)(y_end - y_begin) / n1;
     });

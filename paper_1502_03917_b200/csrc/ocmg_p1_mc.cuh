@@ -10,44 +10,85 @@
 // The reference-order modes keep the reference's exact arithmetic; this mode
 // is its own smoother (its own convergence factor).
 //
-// Pipelining.  Colour q of the sweep at row y reads r on rows y-1..y+1 and
-// writes the same rows; colour q+1 at row y' needs colour q finished on rows
-// <= y'+2.  So one CTA streams its rows bottom to top, running colour q on
-// row s - 3q at step s: the 7 colour-rows of a step touch disjoint rows and
-// are independent, one __syncthreads per step.  Warp q owns colour q, lane m
-// its m-th vertex in the row (vertices of one colour are 7 columns apart).
-// The live rows (s-19 .. s+1) sit in a 24-row shared-memory ring of
-// (state, adjoint) pairs, so every neighbour is one 16-byte access and a
-// vertex's two unknown updates share one load and one store of its
-// neighbourhood; rows are prefetched PF steps ahead into registers, row
-// s-20 is final and leaves.
+// Pipelining.  Colour q at row y reads r on rows y-1..y+1 and writes the
+// same rows; colour q+1 at row y' needs colour q finished on rows <= y'+2.
+// A CTA streams its rows bottom to top in supersteps of K = 2 rows: colour
+// q updates rows K S - C q + {0, 1} at superstep S (skew C = K + 2 rows), so
+// the 14 colour-rows of a superstep touch disjoint rows and are independent;
+// one __syncthreads per superstep.  Warp q owns colour q; its lane m the
+// m-th vertex of that colour in each of the two rows (7 columns apart), so
+// every lane has two independent vertex updates per superstep.
 //
-// Decomposition.  A CTA owns W columns x seg_h rows.  The valid region of r
-// shrinks by 2 columns (rows) per colour, so it loads its tile plus a halo of
-// H = 14 on every side, recomputes the halo (only where the result can reach
-// the tile: margin 2(6-q)+1 for colour q) and writes only its own tile.
-// Halos are read from r_in and the tile is written to r_out (out of place:
-// neighbours read what this CTA overwrites); x is updated in place by the
-// owning CTA.  Two CTAs per SM (79 KB of shared memory each); strips get base
-// or base+1 row segments so the grid fills the SMs once.
+// Shared memory (one CTA per SM, 8 warps, 211 KB):
+//  * the r ring: 34 rows of (state, adjoint) pairs over the tile plus halo;
+//    a neighbour is one 16-byte access and a vertex's two unknown updates
+//    share one load and one store of its neighbourhood;
+//  * the x ring: the owned columns of the same rows.  x is loaded with the
+//    row (coalesced) and written back with it when the row is final, so a
+//    lane never touches x in global memory (a warp's vertices are 56 bytes
+//    apart: 13 cache lines per access when it did);
+//  * the class rows (3, c) of the boundary columns.
+// Rows arrive by cp.async two supersteps ahead (zero-filled outside the
+// domain) and leave, r to r_out and x in place, LAG = 27 rows behind.
+//
+// Boundary classes.  In interior rows only columns 0..2 and n1-3..n1-1 have
+// other classes.  Their vertices belong to the eighth warp: its lane
+// (side, q, i) takes the (at most one) vertex of colour-warp q, row i in the
+// three columns at that side, with the class row from shared memory, while
+// the colour warps run the interior class on every lane (lanes outside the
+// computed region discard their results).  So the edge strips cost what the
+// others do.  The top and bottom three rows read per-lane class rows from
+// the global table.
+//
+// Decomposition.  A CTA owns W = 176 columns (balanced strips) x seg_h rows.
+// The valid region of r shrinks by 2 columns (rows) per colour, so it loads
+// its tile plus a halo of H = 14 on every side, recomputes the halo (only
+// where the result can reach the tile: margin 2(6-q)+1 for colour q) and
+// writes only its own tile.  Halos are read from r_in and the tile is
+// written to r_out (out of place: neighbours read what this CTA
+// overwrites); x is updated in place by the owning CTA.  Strips get base or
+// base+1 row segments so the grid fills the SMs once.
 #pragma once
 
 #include "ocmg_p1.cuh"
 
 namespace ocmg {
 namespace mcs {
+#ifndef MCS_K
+#define MCS_K 2
+#endif
+#ifndef MCS_D
+#define MCS_D 2
+#endif
+#ifndef MCS_W
+#define MCS_W 176
+#endif
 constexpr int NC = kMcColours;     // 7
 constexpr int H = 2 * NC;          // 2 columns (rows) per colour
-constexpr int RING = 3 * (NC - 1) + 6;  // rows s-20 .. s+2 (+1 spare)
-constexpr int NWARP = NC;          // one warp per colour of the sweep
-constexpr int NT = 32 * NWARP;
-constexpr int PF = 4;              // row prefetch depth (steps)
-constexpr int W = 176;             // owned columns per CTA
-constexpr int STRIDE = W + 2 * H + 2;  // + guard column each side
-constexpr int SMEM = RING * STRIDE * 16;
-constexpr int STORE_LAG = 3 * (NC - 1) + 2;  // row s - STORE_LAG is final at step s
+constexpr int K = MCS_K;           // rows per colour and superstep
+constexpr int C = K + 2;           // row skew between consecutive colours
+// superstep S stores rows Ylo + K S - LAG + i (i < K): final once colour 6
+// has passed them
+constexpr int LAG = (NC - 1) * C + 1 + K;
+constexpr int D = MCS_D;           // cp.async prefetch distance (supersteps)
+// live rows: the K leaving (LAG behind) .. the K D + K rows in flight
+constexpr int RING = K * D + K + LAG + 1;
+constexpr int NT = 32 * (NC + 1);  // 7 colour warps + the boundary-column warp
+constexpr int W = MCS_W;           // owned columns per CTA (at most)
+constexpr int STRIDE = W + 2 * H + 2;  // r ring row: columns xl-1 .. xr
+constexpr int RS = STRIDE * 16;    // r ring row bytes: (state, adjoint) pairs
+constexpr int XS = W * 16;         // x ring row bytes: owned columns' pairs
+constexpr int CROW = 30;           // class row: W (14), A (14), 1/n_diag, pad
+// r ring, x ring (slots of the r ring, owned columns), the class rows (3, c)
+// of boundary columns in interior rows.  Lanes outside the tile read (and
+// discard) up to 19 r entries past a row end, inside the x ring at worst.
+constexpr int X_OFF = RING * RS;
+constexpr int CLS_OFF = X_OFF + RING * XS;
+constexpr int SMEM = CLS_OFF + 7 * 2 * CROW * 8;
+constexpr int NLD = (2 * STRIDE + 2 * W + NT - 1) / NT;  // row-load entries per thread
+constexpr int NST = (2 * W + NT - 1) / NT;               // row-store pairs per thread
 static_assert((W + 2 * H + 6) / 7 <= 31, "one warp per colour-row, lane 31 free");
-static_assert(2 * STRIDE <= 2 * NT && 2 * W <= 2 * NT, "two values per thread");
+static_assert(SMEM + 1024 <= 228 * 1024, "one CTA per SM");
 
 // one unknown (field f of the vertex) in the multicolour sweep's arithmetic:
 //   p = (sum_d W_d r_S(d) + sum_d W_{7+d} r_A(d)) * (1 / n_diag),
@@ -71,26 +112,41 @@ __device__ __forceinline__ double node_update(double2 (&v)[7], const double *c) 
                             __fma_rn(-c[21 + d], p, v[d].y));
     return p;
 }
-// the same update with the coefficients read from shared memory by explicit
-// 16-byte ld.shared (asm volatile: one load per use, never hoisted into
-// registers -- the 58 interior coefficients would not fit beside the
-// neighbourhood at 2 CTAs per SM, and indexed LDC from the parameter bank
-// was a fifth of all instructions); cs: shared-memory address of a 30-double
-// row (W 14, A 14, 1/n_diag, pad), 16-byte aligned
-__device__ __forceinline__ double2 lds2(unsigned a) {
-    double2 v;
-    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
-    return v;
+
+// The interior class (3,3) row has the stencil's symmetry bitwise: M has a
+// centre and one neighbour value, K a centre, an axis and a diagonal value
+// (d = 0 and 6 are the SW-NE diagonal neighbours, d = 3 the vertex).  So the
+// 58 interior coefficients are 19 distinct doubles: A values {m1, m0, kd, ka,
+// k0, -m1/a, -m0/a} (0-6), state-unknown W {M nbr, M centre, K diag, K axis,
+// K centre} (7-11), adjoint-unknown W {K diag, K axis, K centre, M nbr,
+// M centre} (12-16), 1/n_diag state, adjoint (17, 18).  umap(f, i) is the
+// distinct index of slot i (node_update layout) of field f; the host checks
+// every slot against it (mcs_fill_cu).
+constexpr int NU = 19;
+__host__ __device__ constexpr int mcls(int d) { return d == 3 ? 1 : 0; }
+__host__ __device__ constexpr int kcls(int d) { return d == 3 ? 2 : (d == 0 || d == 6) ? 0 : 1; }
+__host__ __device__ constexpr int umap(int f, int i) {
+    return f == 0 ? (i < 7 ? 7 + mcls(i) : i < 14 ? 9 + kcls(i - 7) : i < 21 ? mcls(i - 14)
+                     : i < 28 ? 2 + kcls(i - 21) : 17)
+                  : (i < 7 ? 12 + kcls(i) : i < 14 ? 15 + mcls(i - 7) : i < 21 ? 2 + kcls(i - 14)
+                     : i < 28 ? 5 + mcls(i - 21) : 18);
 }
-__device__ __forceinline__ double node_update_s(double2 (&v)[7], unsigned cs) {
-    double c[30];
+// node_update on the interior class, coefficients from the distinct set
+// (same operations in the same order, hence bit-identical)
+template <int F>
+__device__ __forceinline__ double node_update_u(double2 (&v)[7], const double (&u)[NU]) {
+    double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-    for (int i = 0; i < 15; ++i) {
-        const double2 t = lds2(cs + 16 * i);
-        c[2 * i] = t.x;
-        c[2 * i + 1] = t.y;
+    for (int d = 0; d < 7; ++d) {
+        s0 = __fma_rn(u[umap(F, d)], v[d].x, s0);
+        s1 = __fma_rn(u[umap(F, 7 + d)], v[d].y, s1);
     }
-    return node_update(v, c);
+    const double p = __dmul_rn(__dadd_rn(s0, s1), u[umap(F, 28)]);
+#pragma unroll
+    for (int d = 0; d < 7; ++d)
+        v[d] = make_double2(__fma_rn(-u[umap(F, 14 + d)], p, v[d].x),
+                            __fma_rn(-u[umap(F, 21 + d)], p, v[d].y));
+    return p;
 }
 }  // namespace mcs
 
@@ -98,7 +154,7 @@ struct McsParams {
     int n1, nstrips, base, rem, forward;
     int y_begin, y_end;        // rows this launch owns (a rank's strip; 0, n1)
     int64_t fs_in, fs_out, fs_x;  // field strides of rin / rout / x
-    double ci[2][29];  // interior class (3,3): W row, A row, 1/n_diag per field
+    double cu[mcs::NU];  // interior class (3,3), distinct values (mcs::umap)
     const double *C;   // [49][2][29]: W row, A row, 1/n_diag per (class, field)
     // addressed by global vertex index y*n1+x (+ field * fs_*): rin must hold
     // rows [y_begin-15, y_end+15) of the domain, rout and x rows
@@ -107,193 +163,326 @@ struct McsParams {
     double *rout, *x;
 };
 
-__global__ void __launch_bounds__(mcs::NT, 2)
-    k_p1_mc_sweep(const __grid_constant__ McsParams P) {
+// cp.async of one double (zero-filled when !valid): ring rows are filled
+// without passing through registers
+__device__ __forceinline__ void mcs_cp8(unsigned dst, const double *src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src),
+                 "r"(valid ? 8 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void mcs_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void mcs_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ double2 mcs_lds2(unsigned a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+// node_update with the coefficient row in shared memory (cs: its address,
+// 16-byte aligned; asm volatile keeps the 15 loads next to their use)
+__device__ __forceinline__ double node_update_s(double2 (&v)[7], unsigned cs) {
+    double c[30];
+#pragma unroll
+    for (int i = 0; i < 15; ++i) {
+        const double2 t = mcs_lds2(cs + 16 * i);
+        c[2 * i] = t.x;
+        c[2 * i + 1] = t.y;
+    }
+    return mcs::node_update(v, c);
+}
+
+template <bool FWD>
+__global__ void __launch_bounds__(mcs::NT, 1) k_p1_mc_sweep(const __grid_constant__ McsParams P) {
     using namespace mcs;
-    extern __shared__ double2 ring[];  // [RING][STRIDE] (state, adjoint)
+    extern __shared__ __align__(16) double2 ring[];
     const int tid = threadIdx.x, lane = tid & 31, q = tid >> 5;
     const int n1 = P.n1;
-    const int64_t NI = P.fs_in;
     const int strip = blockIdx.x % P.nstrips, seg = blockIdx.x / P.nstrips;
     const int nseg = P.base + (strip < P.rem ? 1 : 0);
     if (seg >= nseg) return;
     const int rows = P.y_end - P.y_begin;
     const int seg_h = (rows + nseg - 1) / nseg;
-    const int X0 = strip * W, X1 = min(n1, X0 + W);
+    // balanced strips of at most W columns
+    const int X0 = strip * n1 / P.nstrips, X1 = (strip + 1) * n1 / P.nstrips;
     const int Y0 = P.y_begin + seg * seg_h, Y1 = min(P.y_end, Y0 + seg_h);
     if (Y0 >= Y1) return;
     const int xl = max(0, X0 - H), xr = min(n1, X1 + H);
     const int Ylo = max(0, Y0 - H), Yhi = min(n1, Y1 + H);
+    const unsigned sm = (unsigned)__cvta_generic_to_shared(ring);
+    char *const smc = reinterpret_cast<char *>(ring);
+    auto wrap = [](int j) { return j >= RING ? j - RING : j; };
+    {   // class rows (3, c), c = 0..6 = global classes 21..27
+        double *ct = reinterpret_cast<double *>(smc + CLS_OFF);
+        for (int i = tid; i < 7 * 2 * 29; i += NT) ct[(i / 29) * CROW + i % 29] = P.C[21 * 58 + i];
+    }
 
-    // row loader: thread -> two (field, local column incl. guards) entries;
-    // rows are fetched while row <= rmax (rows only grow), the rest are zero
+    // ---- loader: row Ylo-1+m lives in slot m mod RING of both rings.
+    // Entries [0, 2 STRIDE): r (field, local column incl. guards), zero
+    // outside [xl, xr) and for rows past rmax; [2 STRIDE, 2 STRIDE + 2 W): x
+    // (field, owned column), rows Y0 .. Y1-1 only.
     const int rmax = min(Yhi, n1 - 1);
-    int lx[2], lf[2];
-    bool lact[2];
-    double *ldst[2];
+    bool lisx[NLD], lact[NLD], lhas[NLD];
+    unsigned loff[NLD];
+    const double *lp[NLD];  // entry's element in row Ylo-1 (a valid address if inactive)
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
+    for (int e = 0; e < NLD; ++e) {
         const int t = tid + e * NT;
-        lf[e] = t >= STRIDE;
-        const int lc = t - lf[e] * STRIDE;
-        lx[e] = xl - 1 + lc;
-        lact[e] = t < 2 * STRIDE && lx[e] >= xl && lx[e] < xr;
-        ldst[e] = t < 2 * STRIDE ? reinterpret_cast<double *>(ring) + 2 * lc + lf[e] : nullptr;
+        lhas[e] = t < 2 * STRIDE + 2 * W;
+        lisx[e] = t >= 2 * STRIDE;
+        if (!lisx[e]) {
+            const int f = t >= STRIDE, lc = t - f * STRIDE, gx = xl - 1 + lc;
+            lact[e] = gx >= xl && gx < xr;
+            loff[e] = sm + (unsigned)(2 * lc + f) * 8u;
+            lp[e] = P.rin + (lact[e] ? f * P.fs_in + (int64_t)(Ylo - 1) * n1 + gx : 0);
+        } else {
+            const int v = t - 2 * STRIDE, f = v >= W, c = v - f * W, gx = X0 + c;
+            lact[e] = lhas[e] && gx < X1;
+            loff[e] = sm + X_OFF + (unsigned)(2 * c + f) * 8u;
+            lp[e] = P.x + (lact[e] ? f * P.fs_x + (int64_t)(Ylo - 1) * n1 + gx : 0);
+        }
     }
-    auto slot0 = [&](int y) { return ((y - Ylo) % RING + RING) % RING; };
-    auto fetch = [&](int e, int y) -> double {
-        return lact[e] && y >= 0 && y <= rmax
-                   ? __ldg(P.rin + lf[e] * NI + (int64_t)y * n1 + lx[e])
-                   : 0.0;
-    };
-    for (int y = Ylo - 1; y <= Ylo + 1; ++y)
+    int lrow = Ylo - 1;  // next row to load
+    int lslot = 0;       // its slot
+    auto load_row = [&]() {
+        const bool okr = lrow >= 0 && lrow <= rmax, okx = lrow >= Y0 && lrow < Y1;
 #pragma unroll
-        for (int e = 0; e < 2; ++e)
-            if (ldst[e]) ldst[e][2 * STRIDE * slot0(y)] = fetch(e, y);
-    // steady state: one pointer per entry advanced a row per step, and the
-    // rows still to fetch counted down (rows only grow; past rmax: zeros)
-    int lrow = Ylo + 2;  // next row to fetch
-    double pf[PF][2];    // rows s+2 .. s+1+PF in flight
-#pragma unroll
-    for (int i = 0; i < PF; ++i) {
-#pragma unroll
-        for (int e = 0; e < 2; ++e) pf[i][e] = fetch(e, lrow);
+        for (int e = 0; e < NLD; ++e) {
+            if (lhas[e]) {
+                const bool ok = lact[e] && (lisx[e] ? okx : okr);
+                mcs_cp8(loff[e] + (unsigned)lslot * (lisx[e] ? XS : RS), ok ? lp[e] : P.rin, ok);
+            }
+            if (lact[e]) lp[e] += n1;
+        }
         ++lrow;
-    }
-    const double *lsrc[2];
+        lslot = wrap(lslot + 1);
+    };
+    // prologue: rows Ylo-1 .. Ylo+K (superstep 0), then K rows per superstep
+    // 1 .. D-1, one commit group per superstep
+    for (int j = 0; j < K + 2; ++j) load_row();
+    mcs_commit();
+    for (int g = 1; g < D; ++g) {
 #pragma unroll
-    for (int e = 0; e < 2; ++e)
-        lsrc[e] = P.rin + lf[e] * NI + (int64_t)lrow * n1 + lx[e];
-    int lleft = lrow <= rmax ? rmax - lrow + 1 : 0;  // valid rows left to fetch
-    int lslot = slot0(Ylo + 2);  // ring slot of row Ylo+s+2
+        for (int i = 0; i < K; ++i) load_row();
+        mcs_commit();
+    }
 
-    // compute role: warp q = position q of the sweep
-    const int colour = P.forward ? q : NC - 1 - q;
-    const int f0 = P.forward ? 0 : 1;  // first field of each vertex
-    const int mg = 2 * (NC - 1 - q) + 1;  // margin whose result reaches the tile
+    // ---- store role: thread -> NST entries t of each leaving row: t < W an
+    // r pair (column X0+t), W <= t < 2W an x pair (column X0+t-W)
+    bool sact[NST];
+    double *sp[NST];
+    int64_t sfs[NST];
+    unsigned soff[NST], srs[NST];
+#pragma unroll
+    for (int e = 0; e < NST; ++e) {
+        const int t = tid + e * NT;
+        const bool isx = t >= W;
+        const int c = isx ? t - W : t;
+        sact[e] = t < 2 * W && X0 + c < X1;
+        sp[e] = (isx ? P.x : P.rout) + (int64_t)(Ylo - LAG) * n1 + X0 + c;
+        sfs[e] = isx ? P.fs_x : P.fs_out;
+        soff[e] = isx ? sm + X_OFF + (unsigned)c * 16u : sm + (unsigned)(X0 - xl + 1 + c) * 16u;
+        srs[e] = isx ? XS : RS;
+    }
+    int srow = Ylo - LAG;                          // next row to leave
+    int sslot = (RING - (LAG - 1) % RING) % RING;  // its slot
+
+    // ---- compute roles.  Colour warp q = position q of the sweep (colour q
+    // forward, 6 - q backward); at superstep S it updates rows
+    // y_i = Ylo + K S - C q + i (i < K), its lane the vertex at column
+    // xbase + o_i, o_i = (colour - xl - 2 y_i) mod 7.  Vertices of a
+    // boundary column (x < 3 or x > n1-4) in an interior row belong to warp
+    // 7 (the boundary warp): its lane (side, q', i) takes the one vertex of
+    // colour-warp q' row i in the three columns at that side, with the
+    // class row from shared memory.
+    const bool bw = q == NC;
+    const int qq = bw ? (lane % 14) / 2 : q;           // the colour warp emulated
+    const int bi = bw ? lane & 1 : 0;                  // boundary warp: its row i
+    const int side = bw ? (lane < 14 ? 0 : lane < 28 ? 1 : 2) : 0;  // left, right, none
+    const bool bside = bw && ((side == 0 && xl == 0) || (side == 1 && xr == n1));
+    const int colour = FWD ? qq : NC - 1 - qq;
+    const int mg = 2 * (NC - 1 - qq) + 1;  // margin whose result reaches the tile
     const int cxl = max(xl, X0 - mg), cxr = min(xr, X1 + mg);
     const int cyl = max(Ylo, Y0 - mg), cyh = min(Yhi, Y1 + mg);
-    // interior coefficients in shared memory (see node_update_s)
-    __shared__ __align__(16) double sci[2][30];
-    if (tid < 58) sci[tid / 29][tid % 29] = P.ci[tid / 29][tid % 29];
-    const unsigned sci0 = (unsigned)__cvta_generic_to_shared(&sci[f0][0]);
-    const unsigned sci1 = (unsigned)__cvta_generic_to_shared(&sci[1 - f0][0]);
-    // this lane's vertex at step s: row y = Ylo + s - 3q, column
-    // x = xl + o + 7 lane with o = (colour - xl - 2y) mod 7, so o(y+1) = o(y) - 2
-    int y = Ylo - 3 * q;
+    int y = Ylo - C * qq;  // y_0
     int o = (colour - xl - 2 * y) % 7;
     o += o < 0 ? 7 : 0;
-    int sy = slot0(y);
-    const int64_t FX = P.fs_x;
-    double *xrow = P.x + (int64_t)y * n1 + xl + 7 * lane;
     const int xbase = xl + 7 * lane;
-    auto owned = [&](int yy, int xx) {
-        return yy >= Y0 && yy < Y1 && xx >= X0 && xx < X1;
-    };
-    // x of the vertex two steps ahead (row y+2, o - 4 mod 7), both fields
-    double xa[2], xb[2];
-    {
-        const int o1 = o - 2 < 0 ? o + 5 : o - 2;
-        const bool w0 = owned(y, xbase + o), w1 = owned(y + 1, xbase + o1);
+    int sl = (RING - (C * qq) % RING) % RING;  // slot of row y_0 - 1
+    double cu[NU];  // interior coefficients (uniform registers)
 #pragma unroll
-        for (int f = 0; f < 2; ++f) {
-            xa[f] = w0 ? xrow[f * FX + o] : 0.0;
-            xb[f] = w1 ? xrow[f * FX + n1 + o1] : 0.0;
-        }
-    }
+    for (int i = 0; i < NU; ++i) cu[i] = P.cu[i];
+    const unsigned cls_s = sm + CLS_OFF;
+    const int S_end = (Y1 - Ylo + LAG + K - 1) / K;
+    mcs_wait<D - 1>();
     __syncthreads();
-    // store role: thread -> two (field, output column) entries; row
-    // Ylo+s-STORE_LAG leaves at step s, i.e. steps [s_st0, s_st1)
-    const double *ssrc[2];
-    double *sdst[2];
-    bool sact[2];
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-        const int t = tid + e * NT;
-        const int sf = t / W, sx = X0 + (t - sf * W);
-        sact[e] = t < 2 * W && sx < X1;
-        ssrc[e] = reinterpret_cast<const double *>(ring) + 2 * (sx - xl + 1) + sf;
-        sdst[e] = P.rout + sf * P.fs_out + (int64_t)Y0 * n1 + sx;
-    }
-    const int s_st0 = Y0 - Ylo + STORE_LAG, s_st1 = Y1 - Ylo + STORE_LAG;
 
-    const int nsteps = (Yhi - Ylo) + STORE_LAG;
-    for (int s = 0; s < nsteps; ++s) {
-        double lnew[2];
+    for (int S = 0; S < S_end; ++S) {
+        // 1. the rows superstep S + D needs first
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            lnew[e] = lact[e] && lleft > 0 ? __ldg(lsrc[e]) : 0.0;
-            lsrc[e] += n1;
-        }
-        lleft -= lleft > 0 ? 1 : 0;
-        double xcur[2];
-        {
-            const int o2 = o + 3 >= 7 ? o - 4 : o + 3;
-            const bool w2 = owned(y + 2, xbase + o2);
+        for (int i = 0; i < K; ++i) load_row();
+        mcs_commit();
+        // 2. final rows leave (r pairs, x pairs)
 #pragma unroll
-            for (int f = 0; f < 2; ++f) {
-                xcur[f] = xa[f];
-                xa[f] = xb[f];
-                xb[f] = w2 ? xrow[f * FX + 2 * (int64_t)n1 + o2] : 0.0;
+        for (int i = 0; i < K; ++i) {
+            if (srow >= Y0 && srow < Y1) {  // CTA-uniform
+#pragma unroll
+                for (int e = 0; e < NST; ++e)
+                    if (sact[e]) {
+                        const double2 v = mcs_lds2(soff[e] + (unsigned)sslot * srs[e]);
+                        sp[e][0] = v.x;
+                        sp[e][sfs[e]] = v.y;
+                    }
             }
-        }
-        if (s >= s_st0 && s < s_st1) {
-            const int ss = lslot + (RING - 2 - STORE_LAG) % RING;  // slot of row Ylo+s-STORE_LAG
-            const int slot = ss >= RING ? ss - RING : ss;
 #pragma unroll
-            for (int e = 0; e < 2; ++e)
-                if (sact[e]) {
-                    *sdst[e] = ssrc[e][2 * STRIDE * slot];
-                    sdst[e] += n1;
+            for (int e = 0; e < NST; ++e) sp[e] += n1;
+            ++srow;
+            sslot = wrap(sslot + 1);
+        }
+        // 3. vertex updates (independent: same colour, distance >= 3)
+        auto rrow = [&](int j) {  // r ring row j (slot sl + j) as double2*
+            return reinterpret_cast<double2 *>(smc + wrap(sl + j) * RS);
+        };
+        auto xent = [&](int i, int x) {  // x ring entry of (y_i, x)
+            return reinterpret_cast<double2 *>(smc + X_OFF + wrap(sl + i + 1) * XS) + (x - X0);
+        };
+        auto load_v = [&](int i, int x, double2 (&v)[7]) {
+            const int col = x - xl + 1;
+            const double2 *rb = rrow(i) + col, *rc = rrow(i + 1) + col, *ru = rrow(i + 2) + col;
+            v[0] = rb[-1]; v[1] = rb[0];
+            v[2] = rc[-1]; v[3] = rc[0]; v[4] = rc[1];
+            v[5] = ru[0]; v[6] = ru[1];
+        };
+        auto store_v = [&](int i, int x, const double2 (&v)[7]) {
+            const int col = x - xl + 1;
+            double2 *rb = rrow(i) + col, *rc = rrow(i + 1) + col, *ru = rrow(i + 2) + col;
+            rb[-1] = v[0]; rb[0] = v[1];
+            rc[-1] = v[2]; rc[0] = v[3]; rc[1] = v[4];
+            ru[0] = v[5]; ru[1] = v[6];
+        };
+        auto x_update = [&](int i, int x, double pa, double pb) {
+            double2 *xp = xent(i, x);
+            const double2 xo = *xp;
+            *xp = make_double2(__dadd_rn(xo.x, FWD ? pa : pb), __dadd_rn(xo.y, FWD ? pb : pa));
+        };
+        auto owned = [&](int i, int x) {
+            return (unsigned)(y + i - Y0) < (unsigned)(Y1 - Y0) &&
+                   (unsigned)(x - X0) < (unsigned)(X1 - X0);
+        };
+        auto in_rows = [&](int i) { return (unsigned)(y + i - cyl) < (unsigned)(cyh - cyl); };
+        auto int_row = [&](int i) { return (unsigned)(y + i - 3) <= (unsigned)(n1 - 7); };
+        auto int_col = [&](int x) { return (unsigned)(x - 3) <= (unsigned)(n1 - 7); };
+        if (!bw) {
+            int xi[K];
+            bool act[K];
+            bool allint = true;
+#pragma unroll
+            for (int i = 0; i < K; ++i) {
+                const int oi = (o - 2 * i + 7 * K) % 7;
+                xi[i] = xbase + oi;
+                act[i] = in_rows(i) && (unsigned)(xi[i] - cxl) < (unsigned)(cxr - cxl);
+                allint = allint && int_row(i);
+                // boundary columns of interior rows: the boundary warp's
+                act[i] = act[i] && (!int_row(i) || int_col(xi[i]));
+            }
+            if (allint) {  // warp-uniform: every computed lane has the interior class
+                double2 v[K][7];
+#pragma unroll
+                for (int i = 0; i < K; ++i) load_v(i, xi[i], v[i]);
+                double pa[K], pb[K];  // first / second unknown in sweep order
+#pragma unroll
+                for (int i = 0; i < K; ++i) pa[i] = node_update_u<FWD ? 0 : 1>(v[i], cu);
+#pragma unroll
+                for (int i = 0; i < K; ++i) pb[i] = node_update_u<FWD ? 1 : 0>(v[i], cu);
+#pragma unroll
+                for (int i = 0; i < K; ++i)
+                    if (act[i]) {
+                        store_v(i, xi[i], v[i]);
+                        if (owned(i, xi[i])) x_update(i, xi[i], pa[i], pb[i]);
+                    }
+            } else {  // a boundary row: per-lane class rows from the global table
+#pragma unroll
+                for (int i = 0; i < K; ++i) {
+                    if (!in_rows(i)) continue;  // warp-uniform
+                    double2 v[7];
+                    load_v(i, xi[i], v);
+                    double pa, pb;
+                    if (int_row(i)) {
+                        pa = node_update_u<FWD ? 0 : 1>(v, cu);
+                        pb = node_update_u<FWD ? 1 : 0>(v, cu);
+                    } else {
+                        const int xc = min(max(xi[i], 0), n1 - 1);
+                        const int yc = min(max(y + i, 0), n1 - 1);
+                        const double *Cc =
+                            P.C + (7 * p1_axis_class(yc, n1) + p1_axis_class(xc, n1)) * 58;
+                        pa = node_update(v, Cc + (FWD ? 0 : 29));
+                        pb = node_update(v, Cc + (FWD ? 29 : 0));
+                    }
+                    if (act[i]) {
+                        store_v(i, xi[i], v);
+                        if (owned(i, xi[i])) x_update(i, xi[i], pa, pb);
+                    }
                 }
-        }
-        const int x = xbase + o;
-        if (y >= cyl && y < cyh && x >= cxl && x < cxr) {
-            const int c0 = x - xl + 1;
-            const int sb = sy == 0 ? RING - 1 : sy - 1;
-            const int su = sy == RING - 1 ? 0 : sy + 1;
-            double2 *rb = ring + sb * STRIDE + c0, *rc = ring + sy * STRIDE + c0,
-                    *ru = ring + su * STRIDE + c0;
-            double2 *const adr[7] = {rb - 1, rb, rc - 1, rc, rc + 1, ru, ru + 1};
-            double2 v[7];
-#pragma unroll
-            for (int d = 0; d < 7; ++d) v[d] = *adr[d];
-            double p[2];
-            if (y >= 3 && y <= n1 - 4 && x >= 3 && x <= n1 - 4) {
-                // coefficients straight from the parameter bank (indexed LDC:
-                // the constant cache, not the shared-memory pipe)
-                p[f0] = node_update_s(v, sci0);
-                p[1 - f0] = node_update_s(v, sci1);
-            } else {
-                const int cls = 7 * p1_axis_class(y, n1) + p1_axis_class(x, n1);
-                p[f0] = node_update(v, P.C + (cls * 2 + f0) * 29);
-                p[1 - f0] = node_update(v, P.C + (cls * 2 + 1 - f0) * 29);
             }
-#pragma unroll
-            for (int d = 0; d < 7; ++d) *adr[d] = v[d];
-            if (owned(y, x)) {
-                xrow[o] = __dadd_rn(xcur[0], p[0]);
-                xrow[FX + o] = __dadd_rn(xcur[1], p[1]);
+        } else if (bside) {
+            // this lane's vertex: row y_bi of colour warp qq, the column in
+            // 0..2 (left) or n1-3..n1-1 (right) with that colour, if any
+            const int yb = y + bi;
+            const int c0 = side == 0 ? 0 : n1 - 3;
+            const int ob = ((colour - 2 * yb - c0) % 7 + 7) % 7;  // column offset from c0
+            const int xb = c0 + ob;
+            if (ob < 3 && in_rows(bi) && int_row(bi) &&
+                (unsigned)(xb - cxl) < (unsigned)(cxr - cxl)) {
+                double2 v[7];
+                load_v(bi, xb, v);
+                const unsigned cs = cls_s + (unsigned)(p1_axis_class(xb, n1) * 2) * (CROW * 8);
+                const double pa = node_update_s(v, cs + (FWD ? 0 : CROW * 8));
+                const double pb = node_update_s(v, cs + (FWD ? CROW * 8 : 0));
+                store_v(bi, xb, v);
+                if (owned(bi, xb)) x_update(bi, xb, pa, pb);
             }
         }
-#pragma unroll
-        for (int e = 0; e < 2; ++e)
-            if (ldst[e]) ldst[e][2 * STRIDE * lslot] = pf[0][e];
-#pragma unroll
-        for (int i = 0; i + 1 < PF; ++i) {
-            pf[i][0] = pf[i + 1][0];
-            pf[i][1] = pf[i + 1][1];
-        }
-        pf[PF - 1][0] = lnew[0];
-        pf[PF - 1][1] = lnew[1];
-        // advance: row y+1
-        lslot = lslot + 1 == RING ? 0 : lslot + 1;
-        sy = sy + 1 == RING ? 0 : sy + 1;
-        ++y;
-        xrow += n1;
-        o = o - 2 < 0 ? o + 5 : o - 2;
+        // advance K rows
+        y += K;
+        sl = wrap(sl + K);
+        o = (o - 2 * K + 7 * K) % 7;
+        mcs_wait<D - 1>();
         __syncthreads();
     }
+    mcs_wait<0>();
+}
+
+// host side: the distinct interior values from ci58 = [state row (29),
+// adjoint row (29)] (node_update layout); false if a slot differs bitwise
+// from its distinct value (the symmetry mcs::umap assumes does not hold)
+inline bool mcs_fill_cu(double (&cu)[mcs::NU], const double *ci58) {
+    bool set[mcs::NU] = {};
+    for (int f = 0; f < 2; ++f)
+        for (int i = 0; i < 29; ++i) {
+            const int u = mcs::umap(f, i);
+            if (!set[u]) cu[u] = ci58[29 * f + i], set[u] = true;
+            if (std::memcmp(&cu[u], &ci58[29 * f + i], sizeof(double)) != 0) return false;
+        }
+    for (bool b : set)
+        if (!b) return false;
+    return true;
+}
+
+inline void mcs_set_smem() {
+    OCMG_CUDA(cudaFuncSetAttribute(k_p1_mc_sweep<true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, mcs::SMEM));
+    OCMG_CUDA(cudaFuncSetAttribute(k_p1_mc_sweep<false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, mcs::SMEM));
+}
+inline void mcs_launch(const McsParams &P, int grid, cudaStream_t s) {
+    OCMG_REQUIRE(((uintptr_t)P.rin & 7) == 0 && ((uintptr_t)P.rout & 7) == 0 &&
+                     ((uintptr_t)P.x & 7) == 0,
+                 "vectors must be 8-byte aligned");
+    if (P.forward)
+        OCMG_LAUNCH(k_p1_mc_sweep<true>, grid, mcs::NT, mcs::SMEM, s, P);
+    else
+        OCMG_LAUNCH(k_p1_mc_sweep<false>, grid, mcs::NT, mcs::SMEM, s, P);
 }
 
 // host-side launch geometry: strips of W columns; base or base+1 row
@@ -305,10 +494,10 @@ struct McsPlan {
 inline McsPlan mcs_plan(int n1, int sm_count, int rows = -1) {
     McsPlan p;
     if (rows < 0) rows = n1;
-    p.nstrips = (n1 + mcs::W - 1) / mcs::W;
-    // segments much shorter than the pipeline fill (2H + STORE_LAG rows) waste steps
+    p.nstrips = (n1 + mcs::W - 1) / mcs::W;  // balanced widths <= W (kernel)
+    // segments much shorter than the pipeline fill (H + STORE_LAG rows) waste steps
     const int max_seg = std::max(1, rows / 24);
-    const int total = std::max(p.nstrips, std::min(2 * sm_count, p.nstrips * max_seg));
+    const int total = std::max(p.nstrips, std::min(sm_count, p.nstrips * max_seg));
     p.base = total / p.nstrips;
     p.rem = total % p.nstrips;
     p.grid = p.nstrips * (p.base + (p.rem ? 1 : 0));
