@@ -651,7 +651,7 @@ void do_prolong_add(const ocmg_transfer *t, const double *c, double *xf,
         if (fyhi < 0) fyhi = nf1;
         const int crows = std::min(t->nc1, (fyhi + 1) >> 1) - (fylo >> 1);
         if (crows <= 0) return;
-        const dim3 g((nf1 + kTX - 1) / kTX, (crows + kTY * kRPT - 1) / (kTY * kRPT));
+        const dim3 g((nf1 + kTX - 1) / kTX, (crows + kTY * kPRPT - 1) / (kTY * kPRPT));
         if (fylo == 0 && fyhi == nf1)
             OCMG_LAUNCH(k_p1_prolong_add_tiled<true>, g, dim3(kTX, kTY), 0, s, t->nc1,
                         t->n_fields, c, xf, fylo, fyhi);

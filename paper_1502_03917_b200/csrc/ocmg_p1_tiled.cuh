@@ -18,6 +18,7 @@
 namespace ocmg {
 
 constexpr int kTX = 32, kTY = 8, kRPT = 8;  // block tile: 32 cols x 64 rows
+constexpr int kPRPT = 4;  // prolongation: coarse rows per thread (8 fine rows)
 constexpr int kRing = 3;                     // boundary classes 0..2, n1-3..n1-1
 
 struct P1Coef28 {
@@ -387,46 +388,61 @@ __global__ void __launch_bounds__(kTX *kTY)
 // Prolongation x_f += P c: thread = fine column, 2*kRPT fine rows; even/even
 // vertices copy (1.0*c), edge midpoints average their two ends (lower first)
 template <bool ALL>  // ALL: the whole level (no row-range guards)
-__global__ void __launch_bounds__(kTX *kTY)
+__global__ void __launch_bounds__(kTX *kTY, 3)
     k_p1_prolong_add_tiled(int nc1, int n_fields, const double *__restrict__ c,
                            double *__restrict__ xf, int fylo, int fyhi) {
     // fine rows [fylo, fyhi), walked as coarse rows [fylo/2, (fyhi+1)/2)
     const int nf1 = 2 * nc1 - 1;
     const int fx = blockIdx.x * kTX + threadIdx.x;
     const int cylo = fylo >> 1, cyhi = min(nc1, (fyhi + 1) >> 1);
-    const int cy0 = cylo + (blockIdx.y * kTY + threadIdx.y) * kRPT;  // coarse rows
+    const int cy0 = cylo + (blockIdx.y * kTY + threadIdx.y) * kPRPT;  // coarse rows
     if (fx >= nf1 || cy0 >= cyhi) return;
     const int64_t Nc = (int64_t)nc1 * nc1, Nf = (int64_t)nf1 * nf1;
     const int ox = fx & 1, hx = fx >> 1;
-    const int cend = min(cy0 + kRPT, cyhi);
+    const int cend = min(cy0 + kPRPT, cyhi);
     for (int b = 0; b < n_fields; ++b) {
         const double *cc = c + b * Nc;
         double *xb = xf + b * Nf;
-        // value of the coarse-row interpolant at this fine column
-        const double *q = cc + (int64_t)cy0 * nc1 + hx;
-        double lo = ox ? __dadd_rn(__dmul_rn(0.5, __ldg(q)), __dmul_rn(0.5, __ldg(q + 1)))
-                       : __dmul_rn(1.0, __ldg(q));
-        double a_lo = __ldg(q), b_lo = ox ? __ldg(q + 1) : 0.0;
-#pragma unroll 4
-        for (int cy = cy0; cy < cend; ++cy) {
+        // all loads first (the compiler cannot move row j+1's x load above
+        // row j's store to the same array): the coarse values a (column hx)
+        // and b (hx+1, odd columns) of rows cy0 .. cend, the fine x pairs
+        double a[kPRPT + 1], bb[kPRPT + 1], xe[kPRPT], xo[kPRPT];
+#pragma unroll
+        for (int j = 0; j <= kPRPT; ++j) {
+            const int cy = cy0 + j;
+            const bool in = cy < nc1 && j <= cend - cy0;
+            const double *q = cc + (int64_t)cy * nc1 + hx;
+            a[j] = in ? __ldg(q) : 0.0;
+            bb[j] = in && ox ? __ldg(q + 1) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < kPRPT; ++j) {
+            const int cy = cy0 + j;
             const int64_t fv = (int64_t)(2 * cy) * nf1 + fx;
-            if (ALL || (2 * cy >= fylo && 2 * cy < fyhi)) xb[fv] = __dadd_rn(xb[fv], lo);
+            const bool e = cy < cend && (ALL || (2 * cy >= fylo && 2 * cy < fyhi));
+            const bool o = cy < cend && cy + 1 < nc1 &&
+                           (ALL || (2 * cy + 1 >= fylo && 2 * cy + 1 < fyhi));
+            xe[j] = e ? xb[fv] : 0.0;
+            xo[j] = o ? xb[fv + nf1] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < kPRPT; ++j) {
+            const int cy = cy0 + j;
+            if (cy >= cend) break;
+            const int64_t fv = (int64_t)(2 * cy) * nf1 + fx;
+            // even fine row 2cy: the coarse-row interpolant at this column
+            const double lo = ox ? __dadd_rn(__dmul_rn(0.5, a[j]), __dmul_rn(0.5, bb[j]))
+                                 : __dmul_rn(1.0, a[j]);
+            if (ALL || (2 * cy >= fylo && 2 * cy < fyhi)) xb[fv] = __dadd_rn(xe[j], lo);
             if (cy + 1 < nc1) {
-                const double *qn = cc + (int64_t)(cy + 1) * nc1 + hx;
-                const double a_hi = __ldg(qn), b_hi = ox ? __ldg(qn + 1) : 0.0;
                 // odd fine row 2cy+1: (ox=0) avg of (hx,cy),(hx,cy+1);
                 // (ox=1) diagonal edge (hx,cy)-(hx+1,cy+1)
-                const double mid = ox ? __dadd_rn(__dmul_rn(0.5, a_lo), __dmul_rn(0.5, b_hi))
-                                      : __dadd_rn(__dmul_rn(0.5, a_lo), __dmul_rn(0.5, a_hi));
+                const double mid = ox ? __dadd_rn(__dmul_rn(0.5, a[j]), __dmul_rn(0.5, bb[j + 1]))
+                                      : __dadd_rn(__dmul_rn(0.5, a[j]), __dmul_rn(0.5, a[j + 1]));
                 if (ALL || (2 * cy + 1 >= fylo && 2 * cy + 1 < fyhi))
-                    xb[fv + nf1] = __dadd_rn(xb[fv + nf1], mid);
-                lo = ox ? __dadd_rn(__dmul_rn(0.5, a_hi), __dmul_rn(0.5, b_hi))
-                        : __dmul_rn(1.0, a_hi);
-                a_lo = a_hi;
-                b_lo = b_hi;
+                    xb[fv + nf1] = __dadd_rn(xo[j], mid);
             }
         }
-        (void)b_lo;
     }
 }
 
