@@ -193,7 +193,7 @@ __device__ __forceinline__ void p1_nep_rows(const P1JacCoef &C, int64_t N, int n
     }
 }
 
-__global__ void __launch_bounds__(kTX *kTY)
+__global__ void __launch_bounds__(kTX *kTY, 4)
     k_p1_ne_p_int(int n1, const __grid_constant__ P1JacCoef C,
                   const double *__restrict__ r, double *__restrict__ p) {
     const int lo = kRing, hi = n1 - 1 - kRing;
@@ -283,7 +283,7 @@ __device__ __forceinline__ void p1_neapply_rows(const P1Coef28 &A, int64_t N,
     }
 }
 
-__global__ void __launch_bounds__(kTX *kTY)
+__global__ void __launch_bounds__(kTX *kTY, 3)
     k_p1_ne_apply_int(int n1, const __grid_constant__ P1Coef28 A,
                       const double *__restrict__ p, double *__restrict__ x,
                       double *__restrict__ r) {
