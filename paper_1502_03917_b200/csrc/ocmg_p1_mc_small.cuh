@@ -18,25 +18,32 @@ constexpr int kMcSmallMaxN1 = 65;
 constexpr int kMcGridMaxN1 = 513;
 
 __host__ __device__ constexpr int mc_small_smem(int n1) {
-    return (n1 + 2) * (n1 + 2) * 16;
+    // residual with a zero guard ring, x pairs, the class table [49][2][29]
+    return (n1 + 2) * (n1 + 2) * 16 + n1 * n1 * 16 + 49 * 58 * 8;
 }
 
+// x, r and the class table all in shared memory: the 7 colour phases touch
+// global memory not at all
 __global__ void __launch_bounds__(1024)
     k_p1_mc_small(int n1, int forward, const double *__restrict__ C,
                   double *__restrict__ x, double *__restrict__ r) {
     extern __shared__ double2 g[];  // [(n1+2)^2] (state, adjoint), zero guards
     const int P = n1 + 2;
-    const int64_t N = (int64_t)n1 * n1;
+    const int N = n1 * n1;
+    double2 *const xs = g + P * P;  // [n1^2] (state, adjoint)
+    double *const Cs = reinterpret_cast<double *>(xs + N);  // [49][2][29]
     for (int i = threadIdx.x; i < P * P; i += blockDim.x) {
         const int gy = i / P, gx = i - gy * P;
         const int ix = gx - 1, iy = gy - 1;
         double2 v = make_double2(0.0, 0.0);
         if (ix >= 0 && ix < n1 && iy >= 0 && iy < n1) {
-            const int64_t k = (int64_t)iy * n1 + ix;
+            const int k = iy * n1 + ix;
             v = make_double2(r[k], r[N + k]);
         }
         g[i] = v;
     }
+    for (int i = threadIdx.x; i < N; i += blockDim.x) xs[i] = make_double2(x[i], x[N + i]);
+    for (int i = threadIdx.x; i < 49 * 58; i += blockDim.x) Cs[i] = __ldg(C + i);
     __syncthreads();
     const int per_row = (n1 + 6) / 7;
     const int count = per_row * n1;
@@ -55,13 +62,13 @@ __global__ void __launch_bounds__(1024)
             for (int d = 0; d < 7; ++d) v[d] = *adr[d];
             const int cls = 7 * p1_axis_class(iy, n1) + p1_axis_class(ix, n1);
             double p[2];
-            p[f0] = mcs::node_update(v, C + (cls * 2 + f0) * 29);
-            p[1 - f0] = mcs::node_update(v, C + (cls * 2 + 1 - f0) * 29);
+            p[f0] = mcs::node_update(v, Cs + (cls * 2 + f0) * 29);
+            p[1 - f0] = mcs::node_update(v, Cs + (cls * 2 + 1 - f0) * 29);
 #pragma unroll
             for (int d = 0; d < 7; ++d) *adr[d] = v[d];
-            const int64_t xi = (int64_t)iy * n1 + ix;
-            x[xi] = __dadd_rn(x[xi], p[0]);
-            x[N + xi] = __dadd_rn(x[N + xi], p[1]);
+            const int xi = iy * n1 + ix;
+            const double2 xo = xs[xi];
+            xs[xi] = make_double2(__dadd_rn(xo.x, p[0]), __dadd_rn(xo.y, p[1]));
         }
         __syncthreads();
     }
@@ -69,10 +76,14 @@ __global__ void __launch_bounds__(1024)
         const int gy = i / P, gx = i - gy * P;
         const int ix = gx - 1, iy = gy - 1;
         if (ix >= 0 && ix < n1 && iy >= 0 && iy < n1) {
-            const int64_t k = (int64_t)iy * n1 + ix;
+            const int k = iy * n1 + ix;
             r[k] = g[i].x;
             r[N + k] = g[i].y;
         }
+    }
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        x[i] = xs[i].x;
+        x[N + i] = xs[i].y;
     }
 }
 
