@@ -592,11 +592,11 @@ __device__ __noinline__ void wf_stage_G_fast(const WfCtx *C, int j, int F,
     }
 }
 
-template <bool BWD>
-__device__ __noinline__ void wf_stage_apply_fast(const WfCtx *C, int j, int FP,
-                                                 int which, int bkind,
-                                                 int okind, int rlo, int nrows,
-                                                 double *ebuf) {
+// rows rlo + o .. rlo + o + M - 1 of the apply stage (see below)
+template <bool BWD, int M>
+__device__ __forceinline__ void wf_apply_part(const WfCtx *C, int j, int FP, int which,
+                                              int bkind, int okind, int rlo, int o,
+                                              int nrows, double *ebuf) {
     using namespace wf;
     const int lane = threadIdx.x & 31;
     const bool edge = lane == 0 || lane == 31;
@@ -606,10 +606,10 @@ __device__ __noinline__ void wf_stage_apply_fast(const WfCtx *C, int j, int FP,
     const int64_t N = C->N;
     double *pring = which == 0 ? C->P.ring1 : C->P.ring2;
     const int slot = ixr & (RW - 1);
-    double pv[HR + 2], bv[HR][2], xv[HR];
+    double pv[M + 2], bv[M][2], xv[M];
 #pragma unroll
-    for (int t = 0; t < HR + 2; ++t) {
-        const int i = rlo - 1 + t;
+    for (int t = 0; t < M + 2; ++t) {
+        const int i = rlo + o - 1 + t;
         const double *p =
             i < 0 ? pring + (int64_t)(C->b - 1) * C->ps1 + (int64_t)(REAL - 1) * RW + slot
                   : pring + (int64_t)C->b * C->ps1 + (int64_t)i * RW + slot;
@@ -618,11 +618,11 @@ __device__ __noinline__ void wf_stage_apply_fast(const WfCtx *C, int j, int FP,
             wfd::cp_async16_cg(ebuf + 2 * t,
                                p - slot + ((lane == 0 ? ixr - 2 : ixr + 1) & (RW - 1)));
     }
-    const int64_t L0 = (int64_t)(C->iy0 + rlo) * n1 + ixr;  // actual for FWD
+    const int64_t L0 = (int64_t)(C->iy0 + rlo + o) * n1 + ixr;  // actual for FWD
     const int64_t lstep = BWD ? -n1 : n1;
     const int64_t lin0 = BWD ? N - 1 - L0 : L0;
 #pragma unroll
-    for (int t = 0; t < HR; ++t) {
+    for (int t = 0; t < M; ++t) {
         const int64_t lin = lin0 + t * lstep;
 #pragma unroll
         for (int f = 0; f < 2; ++f)
@@ -630,7 +630,7 @@ __device__ __noinline__ void wf_stage_apply_fast(const WfCtx *C, int j, int FP,
                            ? __ldcg(C->P.r + f * N + lin)
                            : __ldcg(C->P.ringu + (int64_t)C->b * C->psu +
                                     (int64_t)f * ROWS * RW +
-                                    (int64_t)(rlo + t) * RW + slot);
+                                    (int64_t)(rlo + o + t) * RW + slot);
         xv[t] = __ldcg(C->P.x + FP * N + lin);
     }
     wfd::cp_async_wait_all();
@@ -642,8 +642,8 @@ __device__ __noinline__ void wf_stage_apply_fast(const WfCtx *C, int j, int FP,
     auto A0 = [&](int d) { return -a[BWD ? 6 - d : d]; };
     auto A1 = [&](int d) { return -a[14 + (BWD ? 6 - d : d)]; };
 #pragma unroll
-    for (int t = 1; t <= HR; ++t) {
-        const int i = rlo - 1 + t;
+    for (int t = 1; t <= M; ++t) {
+        const int i = rlo + o - 1 + t;
         const double su = __shfl_up_sync(0xffffffffu, pv[t - 1], 1);
         const double sc = __shfl_up_sync(0xffffffffu, pv[t], 1);
         const double dc = __shfl_down_sync(0xffffffffu, pv[t], 1);
@@ -674,6 +674,19 @@ __device__ __noinline__ void wf_stage_apply_fast(const WfCtx *C, int j, int FP,
             if (i < C->nreal) C->P.x[FP * N + lin] = xv[t - 1] + pv[t];
         }
     }
+    __syncwarp();  // ebuf is reused by the next part
+}
+
+// the apply stages on an interior tile, in two halves of HR/2 rows: the
+// loads of all HR rows in flight at once spilled under the 96-register cap,
+// and a spill of a loaded value waits for the load
+template <bool BWD>
+__device__ __noinline__ void wf_stage_apply_fast(const WfCtx *C, int j, int FP,
+                                                 int which, int bkind,
+                                                 int okind, int rlo, int nrows,
+                                                 double *ebuf) {
+    wf_apply_part<BWD, wf::HR / 2>(C, j, FP, which, bkind, okind, rlo, 0, nrows, ebuf);
+    wf_apply_part<BWD, wf::HR / 2>(C, j, FP, which, bkind, okind, rlo, wf::HR / 2, nrows, ebuf);
 }
 
 // warm L2 for the next DRAM-sourced tile (r_entry or x rows, fields f0..f1)

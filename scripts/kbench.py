@@ -36,9 +36,10 @@ out = torch.empty_like(r)
 rc = torch.empty(coarse.n, dtype=torch.float64, device=dev)
 nj = P.make_smoother(sys_, "normal")
 mc = P.make_smoother(sys_, "lsgs", gs_mode="multicolour")
+wfs = P.make_smoother(sys_, "lsgs", gs_mode="wavefront")
 st = torch.cuda.current_stream()
-BYTES = {"residual": 24, "ne_jacobi": 32, "multicolour": 32, "restrict": 10,
-         "prolong": 18}
+BYTES = {"residual": 24, "ne_jacobi": 56, "multicolour": 32, "wavefront": 32,
+         "restrict": 10, "prolong": 18}
 
 
 def fn_for(op):
@@ -49,6 +50,8 @@ def fn_for(op):
         return lambda: nj.sweep(x, r)
     if op == "multicolour":
         return lambda: mc.sweep(x, r)
+    if op == "wavefront":
+        return lambda: wfs.sweep(x, r)
     t = tr
     if op == "restrict":
         return lambda: t.restrict(r, rc)
