@@ -276,6 +276,46 @@ def solve_timing(level, alpha, cycle, coarsest, mode, sine, problem="poisson",
             "seconds": t, "setup_seconds": t_setup}
 
 
+def stokes_l10_solves(level=10):
+    """Config 5: Stokes control L10, alpha in {1e-2, 1e-6}, NE-GS (exact
+    order) and NE-Jacobi (tau 0.35, the reference's Stokes default), V(2,2)
+    to 1e-8; one hierarchy per alpha, assembled once for both smoothers."""
+    import torch
+
+    import paper_1502_03917_b200 as P
+    from paper_1502_03917_b200.multigrid import Multigrid, assemble_hierarchy
+    out = []
+    for alpha in (1e-2, 1e-6):
+        t_setup = time.perf_counter()
+        systems, transfers = assemble_hierarchy("stokes", 1, level, alpha)
+        torch.cuda.synchronize()
+        t_setup = time.perf_counter() - t_setup
+        for smoother in ("lsgs", "normal"):
+            kind = (P.SmootherKind("normal", tau=0.35) if smoother == "normal"
+                    else P.SmootherKind("lsgs"))
+            cfg = P.CycleConfig(smoother=kind, cycle="v", coarsest_level=1,
+                                gs_mode="wavefront")
+            mg = Multigrid(systems, transfers, cfg)
+            f = P.baseline_rhs(mg.finest, 1)
+            mg.solve_to_tolerance(f, tol=1e-8, max_cycles=2)   # graph capture
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            _, hist = mg.solve_to_tolerance(f, tol=1e-8, max_cycles=300)
+            torch.cuda.synchronize()
+            t = time.perf_counter() - t0
+            name = ("NE-Jacobi(tau=0.35)" if smoother == "normal"
+                    else "NE-GS[wavefront]")
+            out.append({"config": f"stokes L{level} alpha={alpha} V(2,2) {name} "
+                                  f"coarsest L1",
+                        "cycles": len(hist), "final_rel_residual": hist[-1],
+                        "convergence_factor": float(hist[-1] ** (1.0 / len(hist))),
+                        "seconds": t, "setup_seconds": t_setup})
+            del mg
+        del systems, transfers
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_strip_arm(args, ws, rank, local):
     """--partition strips (N > 1): ONE L12 system strip-partitioned over the
     ranks (strong scaling).  A step is the ghost exchange (torch.distributed
@@ -521,8 +561,7 @@ def run_gpu_arm(args, ws, rank, local):
             result["solve"] += [solve_timing(5, 1e-4, "v", 1, m, False, "stokes")
                                 for m in ("wavefront", "multicolour")]
             if not args.no_stokes_l10:
-                result["solve"].append(
-                    solve_timing(10, 1e-2, "v", 1, "wavefront", False, "stokes"))
+                result["solve"] += stokes_l10_solves()
             if not args.no_solve_l12:
                 # the exact-order W-cycle is north_star's target run (18
                 # cycles, the reference's count); ~9 s
