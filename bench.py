@@ -232,8 +232,10 @@ def kernel_table(dsys, coarse_sys, transfer, x, r, f, stream, iters, hbm):
         time_events(lambda: nj.sweep(x, r), iters, stream), n)
     add("ne_gs_wavefront", "ne_gs",
         time_events(lambda: gs.sweep(x, r), iters, stream), n)
+    # the cycle driver's form: residual ping-pong, no copy back
+    from paper_1502_03917_b200.smoothers import lsgs_sweep_into
     add("ne_gs_multicolour", "ne_gs",
-        time_events(lambda: mc.sweep(x, r), iters, stream), n)
+        time_events(lambda: lsgs_sweep_into(mc, x, r, res_out), iters, stream), n)
     cg = P.make_smoother(dsys, "cgs", gs_mode="multicolour")
     add("cgs_multicolour", "ne_gs",
         time_events(lambda: cg.sweep(x, r), iters, stream), n)
