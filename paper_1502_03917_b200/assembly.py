@@ -434,6 +434,12 @@ def build_poisson_system(level, alpha):
                        matrix=a, norm_diag=L, mass=mass)
 
 
+# generic levels get a greedy distance-2 colouring (multicolour NE-GS) up to
+# this many rows (host time grows with nnz x row length: ~6 s for the 18.9M
+# rows of Stokes L10)
+COLOURING_MAX_ROWS = 25_000_000
+
+
 def _create_csr_level(problem, a, L, layout, pmask, colouring=True):
     off = np.ascontiguousarray(a.indptr, dtype=np.int64)
     col = np.ascontiguousarray(a.indices, dtype=np.int64)
@@ -444,7 +450,7 @@ def _create_csr_level(problem, a, L, layout, pmask, colouring=True):
     _lib.call("ocmg_level_create_csr", problem, a.shape[0], _lib.hptr(off),
               _lib.hptr(col), _lib.hptr(val), _lib.hptr(Ld),
               len(layout.counts), _lib.hptr(fo), pmask,
-              1 if (colouring and a.shape[0] <= 2_000_000) else 0,
+              1 if (colouring and a.shape[0] <= COLOURING_MAX_ROWS) else 0,
               ctypes.byref(h))
     return _Handle(h, "ocmg_level_destroy")
 
