@@ -183,16 +183,31 @@ __device__ __forceinline__ void prolong_add(int nc1, const double *Xc, double *X
     __syncthreads();
 }
 
-// X = A^-1 B, warp per row (k_coarse_inv arithmetic)
+// X = A^-1 B, warp per row (k_coarse_inv arithmetic), four rows per warp in
+// flight: a row's loads are one L2 round trip, and the rows of a warp used to
+// queue behind each other
 __device__ __forceinline__ void coarse(int n, const double *__restrict__ inv, const double *B, double *X) {
+    constexpr int RW = 4;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int row = warp; row < n; row += nw) {
-        const double *a = inv + (int64_t)row * n;
-        double acc = 0.0;
-        for (int j = lane; j < n; j += 32) acc = fma(__ldcs(a + j), B[j], acc);
+    for (int row0 = warp; row0 < n; row0 += RW * nw) {
+        double acc[RW];
 #pragma unroll
-        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) X[row] = acc;
+        for (int k = 0; k < RW; ++k) acc[k] = 0.0;
+        for (int j = lane; j < n; j += 32) {
+            const double bj = B[j];
+#pragma unroll
+            for (int k = 0; k < RW; ++k) {
+                const int row = row0 + k * nw;
+                if (row < n) acc[k] = fma(__ldg(inv + (int64_t)row * n + j), bj, acc[k]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < RW; ++k) {
+#pragma unroll
+            for (int o = 16; o; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+            const int row = row0 + k * nw;
+            if (lane == 0 && row < n) X[row] = acc[k];
+        }
     }
     __syncthreads();
 }
