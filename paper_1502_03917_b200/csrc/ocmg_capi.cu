@@ -234,6 +234,9 @@ void csr_transpose(int64_t nrows, int64_t ncols, const int64_t *off,
 // ---------------------------------------------------------------------------
 
 constexpr int kBlk = 256;
+// levels up to this side length (L9) take the one-row-per-thread residual
+// and transfer kernels: latency, not bandwidth, sets their time
+constexpr int kSmallN1 = 513;
 
 dim3 p1_interior_grid(int n1) {
     const int m = n1 - 2 * kRing;
@@ -246,6 +249,13 @@ void level_residual(const ocmg_level *lv, const double *x, const double *f,
                     double *r, cudaStream_t s, int ylo = 0, int yhi = -1) {
     if (lv->kind == kP1) {
         if (yhi < 0) yhi = lv->n1;
+        if (lv->n1 <= kSmallN1 && ylo == 0 && yhi == lv->n1) {
+            const int64_t N = (int64_t)lv->n1 * lv->n1;
+            OCMG_LAUNCH(k_p1_residual_all, grid_for(N, kBlk), kBlk, 0, s, lv->n1,
+                        lv->tables.p, x, f, r);
+            OCMG_LAUNCH_CHECK();
+            return;
+        }
         const int rlo = std::max(kRing, ylo), rhi = std::min(lv->n1 - kRing, yhi);
         const int m = lv->n1 - 2 * kRing;
         if (rhi > rlo) {
@@ -634,9 +644,15 @@ void do_restrict(const ocmg_transfer *t, const double *rf, double *rc,
         if (cyhi < 0) cyhi = t->nc1;
         const int m = t->nc1, rows = cyhi - cylo;
         if (rows <= 0) return;
-        const dim3 g((m + kTX - 1) / kTX, (rows + kTY * kRPT - 1) / (kTY * kRPT));
-        OCMG_LAUNCH(k_p1_restrict_tiled, g, dim3(kTX, kTY), 0, s, t->nc1, t->n_fields,
-                    rf, rc, cylo, cyhi);
+        if (m <= kSmallN1) {  // small level: a coarse row per thread
+            const dim3 g((m + kTX - 1) / kTX, (rows + kTY - 1) / kTY);
+            OCMG_LAUNCH(k_p1_restrict_tiled<1>, g, dim3(kTX, kTY), 0, s, t->nc1,
+                        t->n_fields, rf, rc, cylo, cyhi);
+        } else {
+            const dim3 g((m + kTX - 1) / kTX, (rows + kTY * kRPT - 1) / (kTY * kRPT));
+            OCMG_LAUNCH(k_p1_restrict_tiled<kRPT>, g, dim3(kTX, kTY), 0, s, t->nc1,
+                        t->n_fields, rf, rc, cylo, cyhi);
+        }
     } else {
         OCMG_LAUNCH(k_csr_spmv, grid_for(t->nc, kBlk), kBlk, 0, s, 
             t->nc, t->R.off.p, t->R.col.p, t->R.val.p, rf, rc);
@@ -651,13 +667,20 @@ void do_prolong_add(const ocmg_transfer *t, const double *c, double *xf,
         if (fyhi < 0) fyhi = nf1;
         const int crows = std::min(t->nc1, (fyhi + 1) >> 1) - (fylo >> 1);
         if (crows <= 0) return;
-        const dim3 g((nf1 + kTX - 1) / kTX, (crows + kTY * kPRPT - 1) / (kTY * kPRPT));
-        if (fylo == 0 && fyhi == nf1)
-            OCMG_LAUNCH(k_p1_prolong_add_tiled<true>, g, dim3(kTX, kTY), 0, s, t->nc1,
+        const bool all = fylo == 0 && fyhi == nf1;
+        if (nf1 <= kSmallN1 && all) {  // small level: a coarse row per thread
+            const dim3 g((nf1 + kTX - 1) / kTX, (crows + kTY - 1) / kTY);
+            OCMG_LAUNCH((k_p1_prolong_add_tiled<true, 1>), g, dim3(kTX, kTY), 0, s, t->nc1,
                         t->n_fields, c, xf, fylo, fyhi);
-        else
-            OCMG_LAUNCH(k_p1_prolong_add_tiled<false>, g, dim3(kTX, kTY), 0, s, t->nc1,
-                        t->n_fields, c, xf, fylo, fyhi);
+        } else {
+            const dim3 g((nf1 + kTX - 1) / kTX, (crows + kTY * kPRPT - 1) / (kTY * kPRPT));
+            if (all)
+                OCMG_LAUNCH((k_p1_prolong_add_tiled<true, kPRPT>), g, dim3(kTX, kTY), 0, s,
+                            t->nc1, t->n_fields, c, xf, fylo, fyhi);
+            else
+                OCMG_LAUNCH((k_p1_prolong_add_tiled<false, kPRPT>), g, dim3(kTX, kTY), 0, s,
+                            t->nc1, t->n_fields, c, xf, fylo, fyhi);
+        }
     } else {
         OCMG_LAUNCH(k_csr_spmv_add, grid_for(t->nf, kBlk), kBlk, 0, s, 
             t->nf, t->P.off.p, t->P.col.p, t->P.val.p, c, xf);

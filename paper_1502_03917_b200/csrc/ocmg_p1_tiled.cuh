@@ -158,6 +158,29 @@ __global__ void k_p1_residual_ring(int n1, const double *__restrict__ T,
     r[N + q.v] = s1;
 }
 
+// the whole level, one thread per vertex (small levels: one launch and no
+// per-thread row walk); the ring kernel's arithmetic, which the interior
+// kernel reproduces bit for bit
+__global__ void k_p1_residual_all(int n1, const double *__restrict__ T,
+                                  const double *__restrict__ x,
+                                  const double *__restrict__ f,
+                                  double *__restrict__ r) {
+    const int64_t N = (int64_t)n1 * n1;
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= N) return;
+    const int iy = (int)(k / n1), ix = (int)(k - (int64_t)iy * n1);
+    const P1Node q = p1_node(ix, iy, n1);
+    const double *A = T + kP1OffA + q.c * 28;
+    double s0 = -p1_row_dot(q, A, x, N);
+    double s1 = -p1_row_dot(q, A + 14, x, N);
+    if (f) {
+        s0 = __dadd_rn(s0, f[q.v]);
+        s1 = __dadd_rn(s1, f[N + q.v]);
+    }
+    r[q.v] = s0;
+    r[N + q.v] = s1;
+}
+
 // ---------------------------------------------------------------------------
 // NE-Jacobi phase 1: p = (tau * W r) / L
 // ---------------------------------------------------------------------------
@@ -333,14 +356,15 @@ __global__ void k_p1_ne_apply_ring(int n1, const double *__restrict__ T,
 // (2cx+1,2cy) (2cx,2cy+1) (2cx+1,2cy+1) (weights 1/2, centre 1), absent
 // vertices skipped.  Fine row 2cy+1 is the next coarse row's 2cy'-1.
 // ---------------------------------------------------------------------------
+template <int RPT>  // coarse rows per thread (kRPT; 1 on small levels)
 __global__ void __launch_bounds__(kTX *kTY)
     k_p1_restrict_tiled(int nc1, int n_fields, const double *__restrict__ rf,
                         double *__restrict__ rc, int cylo, int cyhi) {
     // coarse rows [cylo, cyhi)
     const int cx = blockIdx.x * kTX + threadIdx.x;
-    const int cy0 = cylo + (blockIdx.y * kTY + threadIdx.y) * kRPT;
+    const int cy0 = cylo + (blockIdx.y * kTY + threadIdx.y) * RPT;
     if (cx >= nc1 || cy0 >= cyhi) return;
-    const int nrows = min(kRPT, cyhi - cy0);
+    const int nrows = min(RPT, cyhi - cy0);
     const int nf1 = 2 * nc1 - 1;
     const int64_t Nc = (int64_t)nc1 * nc1, Nf = (int64_t)nf1 * nf1;
     const bool l = cx > 0, rr = cx < nc1 - 1;
@@ -387,7 +411,7 @@ __global__ void __launch_bounds__(kTX *kTY)
 
 // Prolongation x_f += P c: thread = fine column, 2*kRPT fine rows; even/even
 // vertices copy (1.0*c), edge midpoints average their two ends (lower first)
-template <bool ALL>  // ALL: the whole level (no row-range guards)
+template <bool ALL, int PR>  // ALL: the whole level (no row-range guards); PR coarse rows per thread
 __global__ void __launch_bounds__(kTX *kTY, 3)
     k_p1_prolong_add_tiled(int nc1, int n_fields, const double *__restrict__ c,
                            double *__restrict__ xf, int fylo, int fyhi) {
@@ -395,20 +419,20 @@ __global__ void __launch_bounds__(kTX *kTY, 3)
     const int nf1 = 2 * nc1 - 1;
     const int fx = blockIdx.x * kTX + threadIdx.x;
     const int cylo = fylo >> 1, cyhi = min(nc1, (fyhi + 1) >> 1);
-    const int cy0 = cylo + (blockIdx.y * kTY + threadIdx.y) * kPRPT;  // coarse rows
+    const int cy0 = cylo + (blockIdx.y * kTY + threadIdx.y) * PR;  // coarse rows
     if (fx >= nf1 || cy0 >= cyhi) return;
     const int64_t Nc = (int64_t)nc1 * nc1, Nf = (int64_t)nf1 * nf1;
     const int ox = fx & 1, hx = fx >> 1;
-    const int cend = min(cy0 + kPRPT, cyhi);
+    const int cend = min(cy0 + PR, cyhi);
     for (int b = 0; b < n_fields; ++b) {
         const double *cc = c + b * Nc;
         double *xb = xf + b * Nf;
         // all loads first (the compiler cannot move row j+1's x load above
         // row j's store to the same array): the coarse values a (column hx)
         // and b (hx+1, odd columns) of rows cy0 .. cend, the fine x pairs
-        double a[kPRPT + 1], bb[kPRPT + 1], xe[kPRPT], xo[kPRPT];
+        double a[PR + 1], bb[PR + 1], xe[PR], xo[PR];
 #pragma unroll
-        for (int j = 0; j <= kPRPT; ++j) {
+        for (int j = 0; j <= PR; ++j) {
             const int cy = cy0 + j;
             const bool in = cy < nc1 && j <= cend - cy0;
             const double *q = cc + (int64_t)cy * nc1 + hx;
@@ -416,7 +440,7 @@ __global__ void __launch_bounds__(kTX *kTY, 3)
             bb[j] = in && ox ? __ldg(q + 1) : 0.0;
         }
 #pragma unroll
-        for (int j = 0; j < kPRPT; ++j) {
+        for (int j = 0; j < PR; ++j) {
             const int cy = cy0 + j;
             const int64_t fv = (int64_t)(2 * cy) * nf1 + fx;
             const bool e = cy < cend && (ALL || (2 * cy >= fylo && 2 * cy < fyhi));
@@ -426,7 +450,7 @@ __global__ void __launch_bounds__(kTX *kTY, 3)
             xo[j] = o ? xb[fv + nf1] : 0.0;
         }
 #pragma unroll
-        for (int j = 0; j < kPRPT; ++j) {
+        for (int j = 0; j < PR; ++j) {
             const int cy = cy0 + j;
             if (cy >= cend) break;
             const int64_t fv = (int64_t)(2 * cy) * nf1 + fx;
