@@ -254,7 +254,7 @@ def solve_timing(level, alpha, cycle, coarsest, mode, sine, problem="poisson",
     import paper_1502_03917_b200 as P
     t_setup = time.perf_counter()
     kind = (P.SmootherKind("normal", tau=0.4) if smoother == "normal"
-            else P.SmootherKind(smoother))  # lsgs / cgs
+            else P.SmootherKind(smoother))  # lsgs / cgs / vanka
     cfg = P.CycleConfig(smoother=kind, cycle=cycle,
                         coarsest_level=coarsest, gs_mode=mode)
     mg = P.build_solver(problem, level, alpha, cfg)
@@ -269,7 +269,8 @@ def solve_timing(level, alpha, cycle, coarsest, mode, sine, problem="poisson",
     torch.cuda.synchronize()
     t = time.perf_counter() - t0
     sm_name = ("NE-Jacobi(tau=0.4)" if smoother == "normal"
-               else f"CGS[{mode}]" if smoother == "cgs" else f"NE-GS[{mode}]")
+               else f"CGS[{mode}]" if smoother == "cgs"
+               else "Vanka(tau=0.4)" if smoother == "vanka" else f"NE-GS[{mode}]")
     return {"config": f"{problem} L{level} alpha={alpha} {cycle.upper()}(2,2) "
                       f"{sm_name} coarsest L{coarsest}"
                       + (" y_D=U+sin*sin" if sine else ""),
@@ -629,6 +630,9 @@ def run_gpu_arm(args, ws, rank, local):
             # Stokes control (configs 4 and 5; generic CSR kernels)
             result["solve"] += [solve_timing(5, 1e-4, "v", 1, m, False, "stokes")
                                 for m in ("wavefront", "multicolour")]
+            # Vanka patch smoother, config-4 shape
+            result["solve"].append(solve_timing(5, 1e-4, "v", 1, "wavefront", False,
+                                                "stokes", smoother="vanka"))
             if not args.no_stokes_l10:
                 sv, sk = stokes_l10_solves()
                 result["solve"] += sv

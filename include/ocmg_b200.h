@@ -48,6 +48,8 @@ extern "C" {
 #define OCMG_SMOOTHER_LSGS 1   /* NE-GS      (reference "lsgs")   */
 #define OCMG_SMOOTHER_SLSGS 2  /* fwd + bwd NE-GS ("slsgs")        */
 #define OCMG_SMOOTHER_CGS 3    /* collective GS over vertex pairs ("cgs") */
+#define OCMG_SMOOTHER_VANKA 4  /* multiplicative patch smoother ("vanka"):
+                                  forward pre-, backward post-smoothing */
 
 /* NE-GS execution modes */
 #define OCMG_GS_REFERENCE 0   /* level-scheduled, reference arithmetic (bitwise) */
@@ -165,6 +167,22 @@ int ocmg_prolong_add_rows(const ocmg_transfer *t, const double *c, double *xf,
  * doubles.  *ops: touched entries (nnz). */
 int ocmg_cgs_sweep(const ocmg_level *lv, int mode, double *x, double *r,
                    double *scratch, void *stream, int64_t *ops);
+
+/* Vanka patch smoother (SmootherState with kind "vanka", smoothers.py:87-176,
+ * 205-209; Stokes only).  ocmg_level_set_vanka attaches the patches of a
+ * generic (CSR) level -- the reference's build_vanka_patches output: patch
+ * offsets (n_patches+1), global dof indices, and the local inverses padded
+ * to mmax x mmax (row-major, mmax <= 32) -- and builds the dependency
+ * schedule of the multiplicative sweep (patches whose dofs or residual
+ * downdates share a row keep the reference's patch order).
+ * ocmg_vanka_sweep is kernels.vanka_sweep (kernels.py:99-131) via
+ * smoothers.vanka_sweep (smoothers.py:297-310): forward = patch order, else
+ * reversed; bit-identical to the reference.  *ops: touched entries. */
+int ocmg_level_set_vanka(ocmg_level *lv, int64_t n_patches, int mmax,
+                         const int64_t *offsets, const int64_t *dofs,
+                         const double *inverses);
+int ocmg_vanka_sweep(const ocmg_level *lv, double tau, int forward, double *x,
+                     double *r, void *stream, int64_t *ops);
 
 /* Constant-mode removal of the pressure fields (pressure_mean_projection,
  * assembly.py:381-388); no-op for Poisson. */

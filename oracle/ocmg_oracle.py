@@ -622,6 +622,35 @@ class OracleSmoother:
         return self.lsgs(x, r, False)
 
 
+def vanka_sweep(offsets, dofs, inverses, sizes, A, tau, x, r, forward=True):
+    """kernels.vanka_sweep (kernels.py:99-131): multiplicative patch sweep
+    with damping, in patch order (forward) or reversed; the downdate walks
+    the column view of A (sparse.py ColumnView: CSC, rows ascending).
+    Plain loops (small levels only)."""
+    C = A.tocsc()
+    C.sort_indices()
+    n_patches = offsets.shape[0] - 1
+    order = range(n_patches) if forward else range(n_patches - 1, -1, -1)
+    ops = 0
+    for p in order:
+        lo, m = offsets[p], sizes[p]
+        local_r = [r[dofs[lo + a]] for a in range(m)]
+        local_s = []
+        for a in range(m):
+            acc = 0.0
+            for b in range(m):
+                acc += inverses[p, a, b] * local_r[b]
+            local_s.append(tau * acc)
+        for a in range(m):
+            c = dofs[lo + a]
+            sv = local_s[a]
+            x[c] += sv
+            for t in range(C.indptr[c], C.indptr[c + 1]):
+                r[C.indices[t]] -= C.data[t] * sv
+            ops += C.indptr[c + 1] - C.indptr[c]
+    return ops
+
+
 # ---------------------------------------------------------------------------
 # coarse solve, cycle, solve loops (multigrid.py:67-204)
 # ---------------------------------------------------------------------------

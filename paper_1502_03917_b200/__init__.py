@@ -16,9 +16,11 @@ from .mesh import StructuredMesh
 from .multigrid import (CoarseSolver, CycleConfig, Multigrid, SolveReport,
                         assemble_hierarchy, baseline_rhs, build_solver)
 from .smoothers import (SmootherKind, SmootherState, cgs_sweep, lsgs_sweep,
-                        make_smoother, normal_equation_sweep, slsgs_sweep)
+                        make_smoother, normal_equation_sweep, slsgs_sweep,
+                        vanka_sweep)
 from .transfer import (TransferPair, p1_prolongation, p2_prolongation,
                        system_transfer)
+from .vanka import VankaPatches, build_vanka_patches
 
 __version__ = "0.1.0"
 
@@ -31,5 +33,5 @@ __all__ = [
     "make_smoother",
     "normal_equation_sweep", "p1_class_tables", "p1_prolongation",
     "p2_prolongation", "pressure_mean_projection", "slsgs_sweep",
-    "system_transfer",
+    "system_transfer", "VankaPatches", "build_vanka_patches", "vanka_sweep",
 ]

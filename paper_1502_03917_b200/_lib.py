@@ -23,7 +23,7 @@ OCMG_E_SINGULAR = -3
 OCMG_E_STATE = -4
 
 POISSON, STOKES = 0, 1
-SMOOTHER_IDS = {"normal": 0, "lsgs": 1, "slsgs": 2, "cgs": 3}
+SMOOTHER_IDS = {"normal": 0, "lsgs": 1, "slsgs": 2, "cgs": 3, "vanka": 4}
 GS_MODES = {"reference": 0, "wavefront": 1, "multicolour": 2}
 
 # table sizes, mirrored from csrc/ocmg_p1.cuh and csrc/ocmg_wavefront.cuh
@@ -73,6 +73,8 @@ SIGNATURES = {
     "ocmg_residual_rows": (_I, [_P, _P, _P, _P, _I, _I, _P]),
     "ocmg_cgs_sweep": (_I, [_P, _I, _P, _P, _P, _P, ctypes.POINTER(_I64)]),
     "ocmg_level_set_alpha": (_I, [_P, _D]),
+    "ocmg_level_set_vanka": (_I, [_P, _I64, _I, _P, _P, _P]),
+    "ocmg_vanka_sweep": (_I, [_P, _D, _I, _P, _P, _P, ctypes.POINTER(_I64)]),
     "ocmg_restrict_rows": (_I, [_P, _P, _P, _I, _I, _P]),
     "ocmg_prolong_add_rows": (_I, [_P, _P, _P, _I, _I, _P]),
     "ocmg_mean_project": (_I, [_P, _P, _P]),

@@ -62,6 +62,14 @@ struct ocmg_level {
     Schedule sched[2];  // 0 forward, 1 backward
     Schedule colours;
     bool has_colours = false;
+    // Vanka patches (ocmg_level_set_vanka)
+    int64_t vk_np = 0;
+    int vk_mmax = 0;
+    DevBuf<int64_t> vk_off;
+    DevBuf<int32_t> vk_dofs;
+    DevBuf<double> vk_inv;
+    Schedule vk_sched;  // patches by dependency level, forward order
+    int64_t vk_ops = 0;  // touched entries per sweep (kernels.py:130)
     // structured P1
     int k = 0, n1 = 0;
     double alpha = 0.0;
@@ -325,6 +333,65 @@ void run_schedule(const ocmg_level *lv, const Schedule &S, bool reverse,
                         S.rows.p + lo, lv->A.off.p, lv->A.col.p, lv->A.val.p, lv->W.p,
                         lv->ndiag.p, x, r);
         }
+    }
+    OCMG_LAUNCH_CHECK();
+}
+
+// One dependency level of the Vanka sweep (kernels.py:99-131), a warp per
+// patch (<= 32 dofs, lane a = local dof a): gather r on the patch, the local
+// inverse times it (b in order, separate multiply and add), the damped
+// update, x += s, then the downdates r_j -= A_jc s_c dof by dof (lanes over
+// the entries of column c = row c; rows of one column are distinct), so
+// every r_j receives its terms in the reference's order.  Patches of one
+// level share no row.
+__global__ void k_vanka_level(int cnt, const int32_t *__restrict__ ids,
+                              const int64_t *__restrict__ poff,
+                              const int32_t *__restrict__ dofs,
+                              const double *__restrict__ inv, int mmax,
+                              const int64_t *__restrict__ aoff,
+                              const int32_t *__restrict__ acol,
+                              const double *__restrict__ aval, double tau,
+                              double *__restrict__ x, double *__restrict__ r) {
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= cnt) return;
+    const int p = ids[w];
+    const int64_t lo = poff[p];
+    const int m = (int)(poff[p + 1] - lo);
+    const int c = lane < m ? dofs[lo + lane] : 0;
+    const double lr = lane < m ? r[c] : 0.0;
+    const double *ip = inv + ((int64_t)p * mmax + lane) * mmax;
+    double acc = 0.0;
+    for (int b = 0; b < m; ++b) {
+        const double lb = __shfl_sync(0xffffffffu, lr, b);
+        if (lane < m) acc = __dadd_rn(acc, __dmul_rn(ip[b], lb));
+    }
+    const double s = __dmul_rn(tau, acc);
+    if (lane < m) x[c] = __dadd_rn(x[c], s);
+    for (int a = 0; a < m; ++a) {
+        const double sa = __shfl_sync(0xffffffffu, s, a);
+        const int ca = __shfl_sync(0xffffffffu, c, a);
+        for (int64_t t = aoff[ca] + lane; t < aoff[ca + 1]; t += 32) {
+            const int j = acol[t];
+            r[j] = __dsub_rn(r[j], __dmul_rn(aval[t], sa));
+        }
+        __syncwarp();
+    }
+}
+
+void level_vanka(const ocmg_level *lv, double tau, bool forward, double *x, double *r,
+                 cudaStream_t s) {
+    OCMG_REQUIRE(lv->vk_np > 0, "no Vanka patches on this level (ocmg_level_set_vanka)");
+    const Schedule &S = lv->vk_sched;
+    const int64_t nb = (int64_t)S.off.size() - 1;
+    for (int64_t b = 0; b < nb; ++b) {
+        const int64_t l = forward ? b : nb - 1 - b;
+        const int64_t lo = S.off[l], cnt = S.off[l + 1] - lo;
+        if (!cnt) continue;
+        const int64_t thr = cnt * 32;
+        const int blk = thr < 128 ? (int)thr : 128;
+        OCMG_LAUNCH(k_vanka_level, grid_for(thr, blk), blk, 0, s, (int)cnt, S.rows.p + lo,
+                    lv->vk_off.p, lv->vk_dofs.p, lv->vk_inv.p, lv->vk_mmax, lv->A.off.p,
+                    lv->A.col.p, lv->A.val.p, tau, x, r);
     }
     OCMG_LAUNCH_CHECK();
 }
@@ -691,10 +758,14 @@ void do_prolong_add(const ocmg_transfer *t, const double *c, double *xf,
 // ---------------------------------------------------------------------------
 // cycle driver (multigrid.py:130-159)
 // ---------------------------------------------------------------------------
-void smooth(ocmg_hierarchy *h, int hi, double *x, double *r, cudaStream_t s) {
+void smooth(ocmg_hierarchy *h, int hi, double *x, double *r, cudaStream_t s,
+            bool post = false) {
     ocmg_level *lv = h->levels[hi - 1];
     const ocmg_cycle_config &c = h->cfg;
     switch (c.smoother) {
+    case OCMG_SMOOTHER_VANKA:  // smoothers.py:240-244: backward when post
+        level_vanka(lv, c.tau, !post, x, r, s);
+        break;
     case OCMG_SMOOTHER_NORMAL:
         level_ne_jacobi(lv, c.tau, x, r, h->scratch[hi].p, s);
         break;
@@ -713,12 +784,12 @@ void smooth(ocmg_hierarchy *h, int hi, double *x, double *r, cudaStream_t s) {
 // nu smoothing steps; multicolour sweeps on structured levels ping-pong the
 // residual between r and the level scratch instead of copying it back
 void smooth_n(ocmg_hierarchy *h, int hi, int nu, double *x, double *r,
-              cudaStream_t s) {
+              cudaStream_t s, bool post = false) {
     ocmg_level *lv = h->levels[hi - 1];
     const ocmg_cycle_config &c = h->cfg;
     if (!(lv->kind == kP1 && c.gs_mode == OCMG_GS_MULTICOLOUR &&
           (c.smoother == OCMG_SMOOTHER_LSGS || c.smoother == OCMG_SMOOTHER_SLSGS))) {
-        for (int i = 0; i < nu; ++i) smooth(h, hi, x, r, s);
+        for (int i = 0; i < nu; ++i) smooth(h, hi, x, r, s, post);
         return;
     }
     double *buf[2] = {r, h->scratch[hi].p};
@@ -766,7 +837,7 @@ void cycle_rec(ocmg_hierarchy *h, int hi, double *x, const double *rhs,
     do_prolong_add(tr, corr, x, s);
     level_mean_project(lv, x, s);
     level_residual(lv, x, rhs, r, s);
-    smooth_n(h, hi, h->cfg.nu_post, x, r, s);
+    smooth_n(h, hi, h->cfg.nu_post, x, r, s, true);
 }
 
 // Enable the fused coarse block when the bottom of the hierarchy is
@@ -1003,6 +1074,76 @@ int ocmg_level_set_alpha(ocmg_level *lv, double alpha) {
         OCMG_REQUIRE(lv, "null level");
         OCMG_REQUIRE(alpha > 0.0, "alpha must be positive");
         lv->alpha = alpha;
+    });
+}
+
+int ocmg_level_set_vanka(ocmg_level *lv, int64_t n_patches, int mmax,
+                         const int64_t *offsets, const int64_t *dofs,
+                         const double *inverses) {
+    return guarded([&] {
+        OCMG_REQUIRE(lv && offsets && dofs && inverses, "null argument");
+        OCMG_REQUIRE(lv->kind == kCsr, "Vanka patches need a generic (CSR) level");
+        OCMG_REQUIRE(n_patches > 0 && mmax > 0 && mmax <= 32, "bad patch sizes");
+        const int64_t nd = offsets[n_patches];
+        std::vector<int32_t> d32(nd);
+        for (int64_t i = 0; i < nd; ++i) {
+            OCMG_REQUIRE(dofs[i] >= 0 && dofs[i] < lv->n, "patch dof out of range");
+            d32[i] = (int32_t)dofs[i];
+        }
+        for (int64_t p = 0; p < n_patches; ++p)
+            OCMG_REQUIRE(offsets[p + 1] - offsets[p] >= 1 &&
+                             offsets[p + 1] - offsets[p] <= mmax,
+                         "patch larger than mmax");
+        // the operator's pattern (A symmetric: column c = row c)
+        std::vector<int64_t> aoff(lv->n + 1);
+        std::vector<int32_t> acol(lv->A.nnz);
+        OCMG_CUDA(cudaMemcpy(aoff.data(), lv->A.off.p, aoff.size() * 8, cudaMemcpyDeviceToHost));
+        OCMG_CUDA(cudaMemcpy(acol.data(), lv->A.col.p, acol.size() * 4, cudaMemcpyDeviceToHost));
+        // ASAP levels in patch order: a patch touches its dofs (x, and the
+        // r it gathers) and the rows of their columns (r downdates)
+        std::vector<int32_t> last(lv->n, -1), lev(n_patches);
+        int32_t maxlev = -1;
+        for (int64_t p = 0; p < n_patches; ++p) {
+            int32_t m = -1;
+            for (int64_t i = offsets[p]; i < offsets[p + 1]; ++i) {
+                const int32_t c = d32[i];
+                m = std::max(m, last[c]);
+                for (int64_t t = aoff[c]; t < aoff[c + 1]; ++t) m = std::max(m, last[acol[t]]);
+            }
+            lev[p] = m + 1;
+            for (int64_t i = offsets[p]; i < offsets[p + 1]; ++i) {
+                const int32_t c = d32[i];
+                last[c] = m + 1;
+                for (int64_t t = aoff[c]; t < aoff[c + 1]; ++t) last[acol[t]] = m + 1;
+            }
+            maxlev = std::max(maxlev, m + 1);
+        }
+        Schedule &S = lv->vk_sched;
+        S.off.assign(maxlev + 2, 0);
+        for (int64_t p = 0; p < n_patches; ++p) S.off[lev[p] + 1]++;
+        for (size_t l = 1; l < S.off.size(); ++l) S.off[l] += S.off[l - 1];
+        std::vector<int32_t> rows(n_patches);
+        std::vector<int64_t> fill(S.off.begin(), S.off.end() - 1);
+        for (int64_t p = 0; p < n_patches; ++p) rows[fill[lev[p]]++] = (int32_t)p;
+        S.rows.upload(rows);
+        S.doff.upload(S.off);
+        lv->vk_off.upload(offsets, n_patches + 1);
+        lv->vk_dofs.upload(d32);
+        lv->vk_inv.upload(inverses, n_patches * (int64_t)mmax * mmax);
+        lv->vk_np = n_patches;
+        lv->vk_mmax = mmax;
+        lv->vk_ops = 0;
+        for (int64_t i = 0; i < nd; ++i) lv->vk_ops += aoff[d32[i] + 1] - aoff[d32[i]];
+    });
+}
+
+int ocmg_vanka_sweep(const ocmg_level *lv, double tau, int forward, double *x,
+                     double *r, void *stream, int64_t *ops) {
+    return guarded([&] {
+        OCMG_REQUIRE(lv && x && r, "null argument");
+        OCMG_REQUIRE(tau > 0.0 && tau < 2.0, "damping parameter must lie in (0, 2)");
+        level_vanka(lv, tau, forward != 0, x, r, as_stream(stream));
+        if (ops) *ops = lv->vk_ops;
     });
 }
 
@@ -1282,8 +1423,13 @@ int ocmg_hierarchy_create(int n_levels, ocmg_level *const *levels,
                      "null argument");
         OCMG_REQUIRE(n_levels >= 1, "need at least one smoothed level");
         OCMG_REQUIRE(cfg->smoother >= OCMG_SMOOTHER_NORMAL &&
-                         cfg->smoother <= OCMG_SMOOTHER_CGS,
+                         cfg->smoother <= OCMG_SMOOTHER_VANKA,
                      "unknown smoother kind");
+        if (cfg->smoother == OCMG_SMOOTHER_VANKA)
+            for (int i = 0; i < n_levels; ++i)
+                OCMG_REQUIRE(levels[i]->vk_np > 0 && cfg->tau > 0.0 && cfg->tau < 2.0,
+                             "the patch smoother needs Vanka patches on every level "
+                             "(ocmg_level_set_vanka) and a damping in (0, 2)");
         OCMG_REQUIRE(cfg->smoother != OCMG_SMOOTHER_CGS ||
                          levels[n_levels - 1]->problem == OCMG_POISSON,
                      "collective sweep needs a scalar control system");

@@ -3,9 +3,10 @@
 Same names and semantics as the reference: a ``SmootherState`` binds a kind
 to one level; ``sweep(x, r)`` mutates the iterate and the maintained
 residual in place and accumulates the touched-entry count in ``op_count``.
-Only the normal-equation family is in scope (``normal`` = NE-Jacobi,
-``lsgs`` = NE-GS, ``slsgs``); the collective and patch smoothers are
-outside the hot path.
+All five kinds run on the device: the normal-equation family (``normal`` =
+NE-Jacobi, ``lsgs`` = NE-GS, ``slsgs``), the collective pair smoother
+(``cgs``, Poisson) and the Vanka patch smoother (``vanka``, Stokes; SURVEY.md
+§8(f) ranks 1 and 4).
 
 NE-GS runs in one of three modes (``gs_mode``):
   * ``"wavefront"`` -- reference sweep order; on structured Poisson levels
@@ -24,7 +25,7 @@ from . import _lib
 from ._vec import as_device, back_inplace, zeros
 
 SMOOTHER_NAMES = ("normal", "lsgs", "slsgs", "cgs", "vanka")
-DEVICE_SMOOTHERS = ("normal", "lsgs", "slsgs", "cgs")
+DEVICE_SMOOTHERS = ("normal", "lsgs", "slsgs", "cgs", "vanka")
 GS_MODES = tuple(_lib.GS_MODES)
 
 # damping defaults of the experiment protocol (smoothers.py:25-29)
@@ -66,8 +67,8 @@ def check_applicability(kind, problem):
     if kind.name not in DEVICE_SMOOTHERS:
         raise NotImplementedError(
             f"smoother '{kind.name}' is outside the B200 hot path "
-            "(normal / lsgs / slsgs / cgs only)")
-    if kind.name == "normal" and kind.resolved_tau(problem) is None:
+            "(normal / lsgs / slsgs / cgs / vanka only)")
+    if kind.name in ("normal", "vanka") and kind.resolved_tau(problem) is None:
         raise ValueError(f"smoother '{kind.name}' needs a damping parameter")
 
 
@@ -86,6 +87,15 @@ class SmootherState:
         self.tau = kind.resolved_tau(system.problem)
         self.op_count = 0
         self._update = None
+        self.patches = None
+        if kind.name == "vanka":
+            # smoothers.py:219-223: patches once per system, shared by the
+            # states bound to it
+            from . import vanka
+            if getattr(system, "_vanka", None) is None:
+                system._vanka = vanka.build_vanka_patches(system)
+                vanka.attach(system, system._vanka)
+            self.patches = system._vanka
 
     def _scratch(self):
         if self._update is None:
@@ -96,6 +106,9 @@ class SmootherState:
         """One smoothing step of the bound kind (smoothers.py:226-244);
         ``post`` only matters for the patch smoother."""
         name = self.kind.name
+        if name == "vanka":
+            return vanka_sweep(self, x, r,
+                               order="backward" if post else "forward")
         if name == "cgs":
             return cgs_sweep(self, x, r)
         if name == "normal":
@@ -181,6 +194,25 @@ def cgs_sweep(state, x, r):
     ops = ctypes.c_int64()
     _lib.call("ocmg_cgs_sweep", state.system.handle, _lib.GS_MODES[state.gs_mode],
               _lib.dptr(xd), _lib.dptr(rd), _lib.dptr(state._scratch()),
+              _lib.stream_ptr(), ctypes.byref(ops))
+    state.op_count += ops.value
+    back_inplace(xd, x, xnp)
+    back_inplace(rd, r, rnp)
+    return x, r
+
+
+def vanka_sweep(state, x, r, tau=None, order="forward"):
+    """Multiplicative patch sweep with damping (smoothers.py:298-309 ->
+    kernels.py:99-131), bit-identical to the reference."""
+    if order not in ("forward", "backward"):
+        raise ValueError("order must be 'forward' or 'backward'")
+    if state.patches is None:
+        raise ValueError("the state is not bound to the patch smoother")
+    t = state.tau if tau is None else tau
+    xd, xnp, rd, rnp = _pair(state, x, r)
+    ops = ctypes.c_int64()
+    _lib.call("ocmg_vanka_sweep", state.system.handle, float(t),
+              1 if order == "forward" else 0, _lib.dptr(xd), _lib.dptr(rd),
               _lib.stream_ptr(), ctypes.byref(ops))
     state.op_count += ops.value
     back_inplace(xd, x, xnp)

@@ -135,6 +135,31 @@ def cgs_sweep_fixture(k, alpha, seed):
     np.savez_compressed(os.path.join(OUT, f"sweep_poisson_k{k}_cgs.npz"), **d)
 
 
+def vanka_fixture(k, alpha, seed):
+    """Vanka patch smoother (kernels.py:99-131, smoothers.py:87-176,
+    297-...): the patches of a Stokes level and forward / backward sweeps
+    from the same seeded state as sweeps()."""
+    s = ocmg.assemble_hierarchy("stokes", k - 1, k, alpha)[0][-1]
+    rng = np.random.default_rng(seed)
+    x0 = rng.uniform(-1.0, 1.0, s.n)
+    f = rng.uniform(-1.0, 1.0, s.n)
+    ocmg.pressure_mean_projection(s, x0)
+    r0 = s.residual(x0, f)
+    st = ocmg.make_smoother(s, "vanka")
+    pt = st.patches
+    d = {"x0": x0, "f": f, "r0": r0, "offsets": pt.offsets, "dofs": pt.dofs,
+         "sizes": pt.sizes, "inverses": pt.inverses, "vertex_ids": pt.vertex_ids}
+    x, r = x0.copy(), r0.copy()
+    st.sweep(x, r)
+    d["fwd_x"], d["fwd_r"] = x.copy(), r.copy()
+    st.sweep(x, r, post=True)
+    d["fwdbwd_x"], d["fwdbwd_r"] = x.copy(), r.copy()
+    # the reference's operator (its P2 quadrature leaves ~1e-17 entries
+    # where the exact assembly has zeros): the sweep's own input
+    d.update(csr_dict("A", s.matrix))
+    np.savez_compressed(os.path.join(OUT, f"sweep_stokes_k{k}_vanka.npz"), **d)
+
+
 def reference_protocol(problem, k, alpha, smoother, tag):
     cfg = ocmg.CycleConfig(smoother=ocmg.SmootherKind(smoother))
     mg = ocmg.build_solver(problem, k, alpha, cfg)
@@ -173,6 +198,15 @@ def table_fixture():
 if __name__ == "__main__" and sys.argv[1:] == ["table"]:
     ocmg_mesh.MAX_LEVEL = 12
     table_fixture()
+    sys.exit(0)
+
+if __name__ == "__main__" and sys.argv[1:2] == ["vanka"]:
+    # the Vanka patch smoother (added in round 1)
+    ocmg_mesh.MAX_LEVEL = 12
+    vanka_fixture(3, 1e-4, 12)
+    if sys.argv[2:] != ["sweep"]:
+        baseline("stokes", 4, 1e-4, "vanka", "v", 1, 1, "s4_vanka")
+        baseline("stokes", 5, 1e-4, "vanka", "v", 1, 1, "c4_vanka", keep=1)
     sys.exit(0)
 
 if __name__ == "__main__" and sys.argv[1:] == ["cgs"]:
