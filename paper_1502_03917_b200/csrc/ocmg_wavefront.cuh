@@ -689,21 +689,6 @@ __device__ __noinline__ void wf_stage_apply_fast(const WfCtx *C, int j, int FP,
     wf_apply_part<BWD, wf::HR / 2>(C, j, FP, which, bkind, okind, rlo, wf::HR / 2, nrows, ebuf);
 }
 
-// warm L2 for the next DRAM-sourced tile (r_entry or x rows, fields f0..f1)
-template <bool BWD>
-__device__ __noinline__ void wf_prefetch(const WfCtx *C, int j, int rlo,
-                                         int nrows, int f0, int f1,
-                                         const double *base) {
-    const int ixr = j * wf::CW + (threadIdx.x & 31);
-    for (int t = 0; t < nrows; ++t) {
-        const int iyr = C->iy0 + rlo + t;
-        if (!wf_in(C, ixr, iyr)) continue;
-        for (int f = f0; f <= f1; ++f)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(
-                base + f * C->N + wf_vid<BWD>(C, ixr, iyr)));
-    }
-}
-
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
@@ -796,7 +781,6 @@ k_wavefront(WfParams P) {
                 else
                     wf_stage_G<BWD>(C, j, F1, g1, 0, rlo, ROWS, ebuf);
             }
-            if (c + 2 < P.nch) wf_prefetch<BWD>(C, c + 2, rlo - 1, HR + 2, 0, 1, P.r);
         } else if (stage == 1) {
             const int j = c - LAG_U;
             if (j >= 0 && j < P.nch) {
@@ -804,10 +788,6 @@ k_wavefront(WfParams P) {
                     wf_stage_apply_fast<BWD>(C, j, F1, 0, 0, 0, rlo, ROWS_U, ebuf);
                 else
                     wf_stage_apply<BWD>(C, j, F1, 0, ROWS, 0, 0, rlo, ROWS_U, ebuf);
-            }
-            if (j + 1 >= 0 && j + 1 < P.nch) {
-                wf_prefetch<BWD>(C, j + 1, rlo, HR, 0, 1, P.r);
-                wf_prefetch<BWD>(C, j + 1, rlo, HR, F1, F1, P.x);
             }
         } else if (stage == 2) {
             const int j = c - LAG_G;
@@ -826,8 +806,6 @@ k_wavefront(WfParams P) {
                     wf_stage_apply<BWD>(C, j, F2, 1, ROWS_C2, 1, 1, rlo, ctx.nreal,
                                         ebuf);
             }
-            if (j + 1 >= 0 && j + 1 < P.nch)
-                wf_prefetch<BWD>(C, j + 1, rlo, HR, F2, F2, P.x);
         }
 #ifdef OCMG_WF_PROFILE
         if (lane == 0 && P.prof && c >= 0) {
