@@ -59,6 +59,7 @@ struct ocmg_level {
     // generic CSR
     CsrDev A;
     DevBuf<double> W, L, ndiag;
+    SellDev sell;  // A and W again in SELL-32 (residual, NE-Jacobi)
     Schedule sched[2];  // 0 forward, 1 backward
     Schedule colours;
     bool has_colours = false;
@@ -274,8 +275,9 @@ void level_residual(const ocmg_level *lv, const double *x, const double *f,
         OCMG_LAUNCH(k_p1_residual_ring, grid_for(p1_ring_count(lv->n1, kRing), kBlk),
                     kBlk, 0, s, lv->n1, lv->tables.p, x, f, r, ylo, yhi);
     } else {
-        OCMG_LAUNCH(k_csr_residual, grid_for(lv->n, kBlk), kBlk, 0, s, 
-            lv->n, lv->A.off.p, lv->A.col.p, lv->A.val.p, x, f, r);
+        const SellDev &S = lv->sell;
+        OCMG_LAUNCH(k_sell_residual, grid_for(lv->n, kBlk), kBlk, 0, s, lv->n, S.base.p,
+                    S.len.p, S.col.p, S.val.p, x, f, r);
     }
     OCMG_LAUNCH_CHECK();
 }
@@ -298,10 +300,11 @@ void level_ne_jacobi(const ocmg_level *lv, double tau, double *x, double *r,
         OCMG_LAUNCH(k_p1_ne_apply_ring, grid_for(nring, kBlk), kBlk, 0, s, lv->n1,
                     lv->tables.p, scratch, x, r);
     } else {
-        OCMG_LAUNCH(k_csr_ne_p, grid_for(lv->n, kBlk), kBlk, 0, s, 
-            lv->n, lv->A.off.p, lv->A.col.p, lv->W.p, lv->L.p, tau, r, scratch);
-        OCMG_LAUNCH(k_csr_ne_apply, grid_for(lv->n, kBlk), kBlk, 0, s, 
-            lv->n, lv->A.off.p, lv->A.col.p, lv->A.val.p, scratch, x, r);
+        const SellDev &S = lv->sell;
+        OCMG_LAUNCH(k_sell_ne_p, grid_for(lv->n, kBlk), kBlk, 0, s, lv->n, S.base.p,
+                    S.len.p, S.col.p, S.w.p, lv->L.p, tau, r, scratch);
+        OCMG_LAUNCH(k_sell_ne_apply, grid_for(lv->n, kBlk), kBlk, 0, s, lv->n, S.base.p,
+                    S.len.p, S.col.p, S.val.p, scratch, x, r);
     }
     OCMG_LAUNCH_CHECK();
 }
@@ -964,6 +967,28 @@ int ocmg_level_create_csr(int problem, int64_t n, const int64_t *row_off,
         OCMG_LAUNCH(k_csr_ndiag, grid_for(n, kBlk), kBlk, 0, 0, n, lv->A.off.p,
                     lv->A.val.p, lv->W.p, lv->ndiag.p);
         OCMG_LAUNCH_CHECK();
+        {   // SELL-32 copy of A and W
+            SellDev &S = lv->sell;
+            S.nslices = (n + 31) / 32;
+            std::vector<int64_t> base(S.nslices + 1, 0);
+            for (int64_t sl = 0; sl < S.nslices; ++sl) {
+                int64_t wmax = 0;
+                for (int64_t i = 32 * sl; i < std::min(n, 32 * sl + 32); ++i)
+                    wmax = std::max(wmax, row_off[i + 1] - row_off[i]);
+                base[sl + 1] = base[sl] + 32 * wmax;
+            }
+            const int64_t ent = base[S.nslices];
+            S.base.upload(base);
+            S.len.alloc(n);
+            S.col.alloc(ent);
+            S.val.alloc(ent);
+            S.w.alloc(ent);
+            OCMG_CUDA(cudaMemset(S.col.p, 0, ent * sizeof(int32_t)));
+            OCMG_LAUNCH(k_sell_fill, grid_for(n, kBlk), kBlk, 0, 0, n, lv->A.off.p,
+                        lv->A.col.p, lv->A.val.p, lv->W.p, S.base.p, S.len.p, S.col.p,
+                        S.val.p, S.w.p);
+            OCMG_LAUNCH_CHECK();
+        }
         lv->sched[0] = build_schedule(n, row_off, col, true);
         lv->sched[1] = build_schedule(n, row_off, col, false);
         if (want_colouring) {

@@ -100,6 +100,100 @@ __global__ void k_csr_ne_apply(int64_t n, const int64_t *__restrict__ off,
     r[i] = ri;
 }
 
+// ---------------------------------------------------------------------------
+// SELL-32 (sliced ELLPACK, slice height 32 = a warp): the rows of a slice
+// are padded to the slice's longest row and stored entry-major, so the k-th
+// entries of a warp's 32 rows are 32 consecutive words -- coalesced loads
+// where the thread-per-row CSR kernels read 32 scattered rows.  Each thread
+// still sums its own row in column order and stops at the row's length, so
+// the three kernels below are the CSR kernels' arithmetic bit for bit.
+// ---------------------------------------------------------------------------
+struct SellDev {
+    int64_t nslices = 0;
+    DevBuf<int64_t> base;   // [nslices + 1] first entry of each slice
+    DevBuf<int32_t> len;    // [n] row lengths
+    DevBuf<int32_t> col;    // [entries]
+    DevBuf<double> val, w;  // A and row_scaled, same layout
+};
+
+// slice widths -> bases on the host (tiny), entries scattered on the device
+__global__ void k_sell_fill(int64_t n, const int64_t *__restrict__ off,
+                            const int32_t *__restrict__ col,
+                            const double *__restrict__ val,
+                            const double *__restrict__ w,
+                            const int64_t *__restrict__ base,
+                            int32_t *__restrict__ len, int32_t *__restrict__ scol,
+                            double *__restrict__ sval, double *__restrict__ sw) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t b = off[i], m = off[i + 1] - b;
+    len[i] = (int32_t)m;
+    const int64_t dst = base[i >> 5] + (i & 31);
+    for (int64_t k = 0; k < m; ++k) {
+        scol[dst + 32 * k] = col[b + k];
+        sval[dst + 32 * k] = val[b + k];
+        sw[dst + 32 * k] = w[b + k];
+    }
+}
+
+#define OCMG_SELL_ROW(i, t, k, m)                                             \
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;       \
+    if (i >= n) return;                                                      \
+    const int64_t t##0 = base[i >> 5] + (i & 31);                            \
+    const int m = len[i];
+
+__global__ void k_sell_residual(int64_t n, const int64_t *__restrict__ base,
+                                const int32_t *__restrict__ len,
+                                const int32_t *__restrict__ col,
+                                const double *__restrict__ val,
+                                const double *__restrict__ x,
+                                const double *__restrict__ f,
+                                double *__restrict__ r) {
+    OCMG_SELL_ROW(i, t, k, m)
+    double s = 0.0;
+    for (int k = 0; k < m; ++k) {
+        const int64_t t = t0 + 32 * k;
+        s = __dadd_rn(s, __dmul_rn(val[t], x[col[t]]));
+    }
+    double v = -s;
+    if (f) v = __dadd_rn(v, f[i]);
+    r[i] = v;
+}
+
+__global__ void k_sell_ne_p(int64_t n, const int64_t *__restrict__ base,
+                            const int32_t *__restrict__ len,
+                            const int32_t *__restrict__ col,
+                            const double *__restrict__ w,
+                            const double *__restrict__ L, double tau,
+                            const double *__restrict__ r,
+                            double *__restrict__ p) {
+    OCMG_SELL_ROW(i, t, k, m)
+    double q = 0.0;
+    for (int k = 0; k < m; ++k) {
+        const int64_t t = t0 + 32 * k;
+        q = __dadd_rn(q, __dmul_rn(w[t], r[col[t]]));
+    }
+    p[i] = __ddiv_rn(__dmul_rn(tau, q), L[i]);
+}
+
+__global__ void k_sell_ne_apply(int64_t n, const int64_t *__restrict__ base,
+                                const int32_t *__restrict__ len,
+                                const int32_t *__restrict__ col,
+                                const double *__restrict__ val,
+                                const double *__restrict__ p,
+                                double *__restrict__ x,
+                                double *__restrict__ r) {
+    OCMG_SELL_ROW(i, t, k, m)
+    x[i] = __dadd_rn(x[i], p[i]);
+    double ri = r[i];
+    for (int k = 0; k < m; ++k) {
+        const int64_t t = t0 + 32 * k;
+        ri = __dsub_rn(ri, __dmul_rn(val[t], p[col[t]]));
+    }
+    r[i] = ri;
+}
+#undef OCMG_SELL_ROW
+
 // One dependency level (or colour) of the sequential NE-GS sweep: the rows
 // in `rows` are pairwise at graph distance >= 3, so their updates commute
 // and every r_j still receives its updates in index order.  A is symmetric
