@@ -46,6 +46,14 @@ struct Schedule {  // rows bucketed by dependency level (or colour)
     DevBuf<int32_t> rows;
     std::vector<int64_t> off;
     DevBuf<int64_t> doff;  // device copy of off (one-CTA sweep)
+    std::vector<int32_t> hrows;  // host copy of rows
+    // grouped SELL-32: each group's rows in slices of 32 (last one padded
+    // with row -1), entries entry-major per slice (build_group_sell)
+    bool has_gsell = false;
+    std::vector<int64_t> gslice;  // [ngroups + 1] first slice of each group
+    DevBuf<int32_t> gsrow, gslen, gscol;
+    DevBuf<int64_t> gsbase;
+    DevBuf<double> gsval, gsw;
 };
 
 }  // namespace
@@ -169,6 +177,7 @@ Schedule build_schedule(int64_t n, const int64_t *off, const int64_t *col,
     }
     S.rows.upload(rows);
     S.doff.upload(S.off);
+    S.hrows = std::move(rows);
     return S;
 }
 
@@ -201,7 +210,45 @@ Schedule build_colouring(int64_t n, const int64_t *off, const int64_t *col) {
     for (int64_t i = 0; i < n; ++i) rows[fill[colour[i]]++] = (int32_t)i;
     S.rows.upload(rows);
     S.doff.upload(S.off);
+    S.hrows = std::move(rows);
     return S;
+}
+
+// the grouped SELL-32 copy of a schedule (A, W of the level's CSR)
+void build_group_sell(Schedule &S, int64_t n, const int64_t *row_off,
+                      const CsrDev &A, const double *w) {
+    const int64_t ng = (int64_t)S.off.size() - 1;
+    S.gslice.assign(ng + 1, 0);
+    for (int64_t g = 0; g < ng; ++g)
+        S.gslice[g + 1] = S.gslice[g] + (S.off[g + 1] - S.off[g] + 31) / 32;
+    const int64_t nsl = S.gslice[ng];
+    std::vector<int32_t> srow(nsl * 32, -1);
+    std::vector<int64_t> base(nsl + 1, 0);
+    for (int64_t g = 0; g < ng; ++g)
+        for (int64_t k = S.off[g]; k < S.off[g + 1]; ++k)
+            srow[S.gslice[g] * 32 + (k - S.off[g])] = S.hrows[k];
+    for (int64_t sl = 0; sl < nsl; ++sl) {
+        int64_t wmax = 0;
+        for (int l = 0; l < 32; ++l) {
+            const int32_t i = srow[sl * 32 + l];
+            if (i >= 0) wmax = std::max(wmax, row_off[i + 1] - row_off[i]);
+        }
+        base[sl + 1] = base[sl] + 32 * wmax;
+    }
+    const int64_t ent = base[nsl];
+    S.gsrow.upload(srow);
+    S.gsbase.upload(base);
+    S.gslen.alloc(nsl * 32);
+    S.gscol.alloc(ent);
+    S.gsval.alloc(ent);
+    S.gsw.alloc(ent);
+    OCMG_CUDA(cudaMemset(S.gscol.p, 0, ent * sizeof(int32_t)));
+    OCMG_LAUNCH(k_gsell_fill, grid_for(nsl * 32, 256), 256, 0, 0, nsl * 32, S.gsrow.p,
+                S.gsbase.p, A.off.p, A.col.p, A.val.p, w, S.gslen.p, S.gscol.p,
+                S.gsval.p, S.gsw.p);
+    OCMG_LAUNCH_CHECK();
+    S.has_gsell = true;
+    (void)n;
 }
 
 void upload_csr(CsrDev &C, int64_t nrows, int64_t ncols, const int64_t *off,
@@ -329,6 +376,12 @@ void run_schedule(const ocmg_level *lv, const Schedule &S, bool reverse,
             const int blk = thr < 256 ? (int)thr : 256;
             OCMG_LAUNCH(k_csr_gs_rows_warp, grid_for(thr, blk), blk, 0, s, (int)cnt,
                         S.rows.p + lo, lv->A.off.p, lv->A.col.p, lv->A.val.p, lv->W.p,
+                        lv->ndiag.p, x, r);
+        } else if (S.has_gsell) {
+            const int64_t s0 = S.gslice[l], slots = (S.gslice[l + 1] - s0) * 32;
+            const int blk = slots < 128 ? (int)slots : 128;
+            OCMG_LAUNCH(k_gsell_gs_rows, grid_for(slots, blk), blk, 0, s, slots, s0,
+                        S.gsrow.p, S.gsbase.p, S.gslen.p, S.gscol.p, S.gsval.p, S.gsw.p,
                         lv->ndiag.p, x, r);
         } else {
             const int blk = cnt < 128 ? 32 * (int)((cnt + 31) / 32) : 128;
@@ -994,6 +1047,11 @@ int ocmg_level_create_csr(int problem, int64_t n, const int64_t *row_off,
         if (want_colouring) {
             lv->colours = build_colouring(n, row_off, col);
             lv->has_colours = true;
+        }
+        if (n > kCsrSmallN) {  // grouped SELL for the per-group launches
+            build_group_sell(lv->sched[0], n, row_off, lv->A, lv->W.p);
+            build_group_sell(lv->sched[1], n, row_off, lv->A, lv->W.p);
+            if (want_colouring) build_group_sell(lv->colours, n, row_off, lv->A, lv->W.p);
         }
         lv->partial.alloc(kRedGrid);
         lv->scal.alloc(8);

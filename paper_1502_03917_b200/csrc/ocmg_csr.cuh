@@ -272,6 +272,72 @@ __global__ void k_csr_gs_rows_warp(int cnt, const int32_t *__restrict__ rows,
     }
 }
 
+// grouped SELL-32 (a schedule's groups in slices of 32 rows, see
+// build_group_sell): fill, and one group of the NE-GS sweep with csr_gs_row's
+// arithmetic (bit-identical), matrix loads coalesced over a slice
+__global__ void k_gsell_fill(int64_t nslots, const int32_t *__restrict__ srow,
+                             const int64_t *__restrict__ base,
+                             const int64_t *__restrict__ off,
+                             const int32_t *__restrict__ col,
+                             const double *__restrict__ val,
+                             const double *__restrict__ w, int32_t *__restrict__ slen,
+                             int32_t *__restrict__ scol, double *__restrict__ sval,
+                             double *__restrict__ sw) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= nslots) return;
+    const int32_t i = srow[k];
+    if (i < 0) {
+        slen[k] = 0;
+        return;
+    }
+    const int64_t b = off[i], m = off[i + 1] - b;
+    slen[k] = (int32_t)m;
+    const int64_t dst = base[k >> 5] + (k & 31);
+    for (int64_t t = 0; t < m; ++t) {
+        scol[dst + 32 * t] = col[b + t];
+        sval[dst + 32 * t] = val[b + t];
+        sw[dst + 32 * t] = w[b + t];
+    }
+}
+
+__global__ void k_gsell_gs_rows(int64_t nslots, int64_t slice0,
+                                const int32_t *__restrict__ srow,
+                                const int64_t *__restrict__ base,
+                                const int32_t *__restrict__ slen,
+                                const int32_t *__restrict__ col,
+                                const double *__restrict__ val,
+                                const double *__restrict__ w,
+                                const double *__restrict__ ndiag,
+                                double *__restrict__ x, double *__restrict__ r) {
+    const int64_t k = slice0 * 32 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= slice0 * 32 + nslots) return;
+    const int32_t i = srow[k];
+    if (i < 0) return;
+    const int m = slen[k];
+    const int64_t t0 = base[k >> 5] + (k & 31);
+    double q = 0.0;
+    for (int t = 0; t < m; ++t) {
+        const int64_t e = t0 + 32 * t;
+        q = __dadd_rn(q, __dmul_rn(w[e], r[col[e]]));
+    }
+    const double p = __ddiv_rn(q, ndiag[i]);
+    x[i] = __dadd_rn(x[i], p);
+    constexpr int kB = 8;
+    for (int tb = 0; tb < m; tb += kB) {
+        double rv[kB];
+        int32_t jv[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u)
+            if (tb + u < m) {
+                jv[u] = col[t0 + 32 * (tb + u)];
+                rv[u] = r[jv[u]];
+            }
+#pragma unroll
+        for (int u = 0; u < kB; ++u)
+            if (tb + u < m) r[jv[u]] = __dsub_rn(rv[u], __dmul_rn(val[t0 + 32 * (tb + u)], p));
+    }
+}
+
 // Whole sweep of a small level in one CTA: the groups (dependency levels or
 // colours) in order, __syncthreads between them (one launch instead of one
 // per group -- the coarse levels of a W-cycle are visited thousands of times)
