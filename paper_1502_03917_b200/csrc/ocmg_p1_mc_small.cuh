@@ -3,11 +3,12 @@
 // filling and draining.  Same order and arithmetic (p1_mc_vertex /
 // mcs::node_update), so all three forms are bit-identical.
 //
-//   k <= 6  (n1 <= 65):  k_p1_mc_small -- one CTA, the whole residual in
-//                        shared memory (guard ring of zeros), 7 colour
-//                        phases separated by __syncthreads.
-//   7 <= k <= 9:         k_p1_mc_grid -- one cooperative launch, 7 colour
-//                        phases separated by a grid barrier, in place.
+//   k <= 6  (n1 <= 65):  k_p1_mc_small -- one CTA, the whole residual, x and
+//                        the class table in shared memory, 7 colour phases
+//                        separated by __syncthreads.
+//   k_p1_mc_grid -- one cooperative launch, 7 colour phases separated by a
+//                        grid barrier, in place; kept, but the one-launch
+//                        strip kernel (ocmg_p1_mc.cuh) now runs from k = 7.
 #pragma once
 
 #include "ocmg_p1_mc.cuh"
@@ -15,7 +16,9 @@
 namespace ocmg {
 
 constexpr int kMcSmallMaxN1 = 65;
-constexpr int kMcGridMaxN1 = 513;
+// the cooperative tier is kept but unused: the one-launch strip kernel is
+// faster from L7 up in the cycle (W-cycle L12 37.3 -> 35.4 ms)
+constexpr int kMcGridMaxN1 = 65;
 
 __host__ __device__ constexpr int mc_small_smem(int n1) {
     // residual with a zero guard ring, x pairs, the class table [49][2][29]
