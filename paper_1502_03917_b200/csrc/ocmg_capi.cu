@@ -501,6 +501,10 @@ void level_ne_gs(const ocmg_level *lv, int mode, bool forward, double *x,
             if (p1_mc_sweep(lv, forward, x, r, lv->mc_r.p, s))
                 OCMG_CUDA(cudaMemcpyAsync(r, lv->mc_r.p, sizeof(double) * lv->n,
                                           cudaMemcpyDeviceToDevice, s));
+        } else if (n1 <= kGsSmallMaxN1 && ((uintptr_t)x % 16 | (uintptr_t)r % 16) == 0) {
+            // both exact modes: one CTA, levels separated by barriers
+            OCMG_LAUNCH(k_p1_gs_small, 1, kGsSmallThreads, gs_small_smem(n1), s, n1,
+                        lv->tables.p, forward ? 1 : 0, x, r);
         } else if (mode == OCMG_GS_WAVEFRONT && lv->wf.ready()) {
             lv->wf.sweep(forward, x, r, s);
         } else {
@@ -1103,6 +1107,8 @@ int ocmg_level_create_p1(int k, double alpha, const double *tables,
             // per call: the attribute is per device, and cheap to set
             OCMG_CUDA(cudaFuncSetAttribute(k_p1_mc_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            mc_small_smem(kMcSmallMaxN1)));
+            OCMG_CUDA(cudaFuncSetAttribute(k_p1_gs_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)gs_small_smem(kGsSmallMaxN1)));
             lv->mc_tier = lv->n1 <= kMcSmallMaxN1 ? 0 : lv->n1 <= kMcGridMaxN1 ? 1 : 2;
             if (lv->mc_tier == 1) {
                 int occ = 0;

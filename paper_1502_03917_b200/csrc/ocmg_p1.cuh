@@ -199,6 +199,96 @@ __global__ void k_p1_gs_level(int n1, const double *__restrict__ T, int t,
     p1_gs_unknown(field, ix, iy, n1, T, x, r);
 }
 
+// The whole reference-order sweep of a small level in one CTA: x, r and the
+// class tables are staged in shared memory (cp.async), the 3(n1-1)+8
+// dependency levels are separated by __syncthreads instead of kernel
+// launches, and thread (field, row) owns the one unknown of its mesh row at
+// each level (the mapping of k_p1_gs_level).  Same arithmetic as
+// p1_gs_unknown, so bit-identical to the reference sweep; the scatter reuses
+// the gathered residual (no other unknown of the level touches it).  One
+// level costs ~0.2 us (one dependent add chain + a division + a barrier)
+// where a launch per level, or the banded wavefront kernel, costs 0.7-1.7 us.
+constexpr int kGsSmallMaxN1 = 65;
+constexpr int kGsSmallThreads = 160;  // >= 2 * kGsSmallMaxN1
+inline size_t gs_small_smem(int n1) {
+    return (4 * (size_t)n1 * n1 + kP1TableDoubles) * sizeof(double);
+}
+
+__device__ __forceinline__ void gs_cp16(double *dst, const double *src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+
+__global__ void __launch_bounds__(kGsSmallThreads, 1)
+    k_p1_gs_small(int n1, const double *__restrict__ T, int forward,
+                  double *__restrict__ x, double *__restrict__ r) {
+    extern __shared__ __align__(16) double gs_sm[];
+    const int N = n1 * n1;
+    double *sr = gs_sm, *sx = gs_sm + 2 * N, *sT = gs_sm + 4 * N;
+    // 2N doubles per array: n1 odd => N odd, 2N even, 16-byte chunks
+    for (int i = 2 * threadIdx.x; i < 2 * N; i += 2 * kGsSmallThreads) {
+        gs_cp16(sr + i, r + i);
+        gs_cp16(sx + i, x + i);
+    }
+    static_assert(kP1TableDoubles % 2 == 0, "table size");
+    for (int i = 2 * threadIdx.x; i < kP1TableDoubles; i += 2 * kGsSmallThreads)
+        gs_cp16(sT + i, T + i);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    const int depth = 3 * (n1 - 1) + 8;
+    const int k = threadIdx.x;
+    const int field = k >= n1 ? 1 : 0;
+    const int row = k - field * n1;
+    const bool active = k < 2 * n1;
+    for (int t = 0; t < depth; ++t) {
+        int ix, iy;
+        if (forward) {
+            iy = row;
+            ix = (field ? t - 7 : t) - 2 * iy;
+        } else {
+            const int ixr = (field ? t : t - 7) - 2 * row;
+            ix = n1 - 1 - ixr;
+            iy = n1 - 1 - row;
+        }
+        if (active && ix >= 0 && ix < n1) {
+            const int c = 7 * p1_axis_class(iy, n1) + p1_axis_class(ix, n1);
+            const int v = iy * n1 + ix;
+            const bool l = ix > 0, rr = ix < n1 - 1, dn = iy > 0, up = iy < n1 - 1;
+            const bool ex[7] = {l && dn, dn, l, true, rr, up, rr && up};
+            const int nb[7] = {v - n1 - 1, v - n1, v - 1, v, v + 1, v + n1, v + n1 + 1};
+            double g[14];
+#pragma unroll
+            for (int d = 0; d < 7; ++d) {
+                g[d] = ex[d] ? sr[nb[d]] : 0.0;
+                g[7 + d] = ex[d] ? sr[N + nb[d]] : 0.0;
+            }
+            const double *W = sT + kP1OffW + c * 28 + 14 * field;
+            const double *A = sT + kP1OffA + c * 28 + 14 * field;
+            double s = 0.0;
+#pragma unroll
+            for (int d = 0; d < 7; ++d)
+                if (ex[d]) s = __dadd_rn(s, __dmul_rn(W[d], g[d]));
+#pragma unroll
+            for (int d = 0; d < 7; ++d)
+                if (ex[d]) s = __dadd_rn(s, __dmul_rn(W[7 + d], g[7 + d]));
+            const double p = __ddiv_rn(s, sT[kP1OffND + c * 2 + field]);
+            const int i = field * N + v;
+            sx[i] = __dadd_rn(sx[i], p);
+#pragma unroll
+            for (int d = 0; d < 7; ++d)
+                if (ex[d]) {
+                    sr[nb[d]] = __dsub_rn(g[d], __dmul_rn(A[d], p));
+                    sr[N + nb[d]] = __dsub_rn(g[7 + d], __dmul_rn(A[7 + d], p));
+                }
+        }
+        __syncthreads();
+    }
+    for (int i = 2 * threadIdx.x; i < 2 * N; i += 2 * kGsSmallThreads) {
+        *reinterpret_cast<double2 *>(r + i) = *reinterpret_cast<const double2 *>(sr + i);
+        *reinterpret_cast<double2 *>(x + i) = *reinterpret_cast<const double2 *>(sx + i);
+    }
+}
+
 // One vertex of the multicolour sweep (same formula as mcs::node_update in
 // ocmg_p1_mc.cuh): both of its unknowns in turn -- state then adjoint on a
 // forward sweep, adjoint then state on a backward one -- each

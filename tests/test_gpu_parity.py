@@ -102,6 +102,36 @@ def test_ne_gs_reference_mode_bitwise(prob, k, alpha, order):
     assert np.array_equal(host(rd), ro)
 
 
+@pytest.mark.parametrize("mode", ["reference", "wavefront"])
+def test_ne_gs_exact_small_level_unaligned_views(mode):
+    """Small levels run the one-CTA sweep (16-byte cp.async staging); views at
+    an odd double offset take the launch-per-level (reference) or banded (wavefront, 1e-12) path."""
+    osys, dsys = systems("poisson", 5, 1e-4)
+    x0, f, r0 = inputs(osys, 5)
+    st = P.make_smoother(dsys, "lsgs", gs_mode=mode)
+    res = []
+    for off in (0, 1):
+        xb = torch.zeros(osys.n + 1, dtype=torch.float64, device="cuda")
+        rb = torch.zeros_like(xb)
+        xd, rd = xb[off:off + osys.n], rb[off:off + osys.n]
+        xd.copy_(dev(x0))
+        rd.copy_(dev(r0))
+        P.lsgs_sweep(st, xd, rd, order="forward")
+        P.lsgs_sweep(st, xd, rd, order="backward")
+        res.append((host(xd), host(rd)))
+    xo, ro = x0.copy(), r0.copy()
+    ost = O.OracleSmoother(osys, "lsgs")
+    ost.lsgs(xo, ro, forward=True)
+    ost.lsgs(xo, ro, forward=False)
+    for off, (xh, rh) in enumerate(res):
+        if mode == "wavefront" and off == 1:  # the banded kernel: 1e-12
+            assert rel(xh, xo) < 1e-12
+            assert rel(rh, ro) < 1e-11
+        else:
+            assert np.array_equal(xh, xo)
+            assert np.array_equal(rh, ro)
+
+
 @pytest.mark.parametrize("prob,k,alpha", CASES)
 def test_ne_gs_wavefront_mode(prob, k, alpha):
     """Reference order, delta-form arithmetic: 1e-12 (north_star bar)."""
