@@ -271,14 +271,20 @@ __global__ void __launch_bounds__(kGsSmallThreads, 1)
 #pragma unroll
             for (int d = 0; d < 7; ++d)
                 if (ex[d]) s = __dadd_rn(s, __dmul_rn(W[7 + d], g[7 + d]));
-            const double p = __ddiv_rn(s, sT[kP1OffND + c * 2 + field]);
+            // every shared load before the first store (sr, sx and sT share
+            // one array, so the compiler would not hoist them past a store)
+            double a[14];
+#pragma unroll
+            for (int e = 0; e < 14; ++e) a[e] = A[e];
             const int i = field * N + v;
-            sx[i] = __dadd_rn(sx[i], p);
+            const double xi = sx[i];
+            const double p = __ddiv_rn(s, sT[kP1OffND + c * 2 + field]);
+            sx[i] = __dadd_rn(xi, p);
 #pragma unroll
             for (int d = 0; d < 7; ++d)
                 if (ex[d]) {
-                    sr[nb[d]] = __dsub_rn(g[d], __dmul_rn(A[d], p));
-                    sr[N + nb[d]] = __dsub_rn(g[7 + d], __dmul_rn(A[7 + d], p));
+                    sr[nb[d]] = __dsub_rn(g[d], __dmul_rn(a[d], p));
+                    sr[N + nb[d]] = __dsub_rn(g[7 + d], __dmul_rn(a[7 + d], p));
                 }
         }
         __syncthreads();

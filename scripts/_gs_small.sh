@@ -3,3 +3,4 @@ timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "reference
 echo tests=$? >> gpurun_out/gs_small_tests.log
 timeout 600 python bench.py --steps 3 --warmup 3 --no-stokes-l10 --no-cpu > gpurun_out/gs_small_bench.log 2>&1
 echo bench=$? >> gpurun_out/gs_small_bench.log
+bash scripts/_wfl.sh
