@@ -16,6 +16,7 @@
 #include "ocmg_p1_tiled.cuh"
 #include "ocmg_p1_mc.cuh"
 #include "ocmg_p1_mc_small.cuh"
+#include "ocmg_p1_gsdiag.cuh"
 #include "ocmg_subcycle.cuh"
 #include "ocmg_cgs.cuh"
 #include "ocmg_cgs_mc.cuh"
@@ -505,6 +506,14 @@ void level_ne_gs(const ocmg_level *lv, int mode, bool forward, double *x,
             // both exact modes: one CTA, levels separated by barriers
             OCMG_LAUNCH(k_p1_gs_small, 1, kGsSmallThreads, gs_small_smem(n1), s, n1,
                         lv->tables.p, forward ? 1 : 0, x, r);
+        } else if (n1 >= gsd::kMinN1 && n1 <= gsd::kMaxN1) {
+            // both exact modes: one CTA, anti-diagonal ring of r
+            const int nt = 2 * gsd::per_field(n1);
+            const size_t sm = gsd::smem(n1);
+            if (forward)
+                OCMG_LAUNCH((k_p1_gs_diag<320, gsd::kRing, false>), 1, nt, sm, s, n1, lv->tables.p, x, r);
+            else
+                OCMG_LAUNCH((k_p1_gs_diag<320, gsd::kRing, true>), 1, nt, sm, s, n1, lv->tables.p, x, r);
         } else if (mode == OCMG_GS_WAVEFRONT && lv->wf.ready()) {
             lv->wf.sweep(forward, x, r, s);
         } else {
@@ -1109,6 +1118,13 @@ int ocmg_level_create_p1(int k, double alpha, const double *tables,
                                            mc_small_smem(kMcSmallMaxN1)));
             OCMG_CUDA(cudaFuncSetAttribute(k_p1_gs_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)gs_small_smem(kGsSmallMaxN1)));
+            {
+                const int gsm = (int)gsd::smem(gsd::kMaxN1);
+                OCMG_CUDA(cudaFuncSetAttribute(k_p1_gs_diag<320, gsd::kRing, false>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, gsm));
+                OCMG_CUDA(cudaFuncSetAttribute(k_p1_gs_diag<320, gsd::kRing, true>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, gsm));
+            }
             lv->mc_tier = lv->n1 <= kMcSmallMaxN1 ? 0 : lv->n1 <= kMcGridMaxN1 ? 1 : 2;
             if (lv->mc_tier == 1) {
                 int occ = 0;

@@ -132,6 +132,26 @@ def test_ne_gs_exact_small_level_unaligned_views(mode):
             assert np.array_equal(rh, ro)
 
 
+@pytest.mark.parametrize("k", [7, 8])
+@pytest.mark.parametrize("order", ["forward", "backward"])
+@pytest.mark.parametrize("mode", ["reference", "wavefront"])
+def test_ne_gs_exact_mid_levels_bitwise(k, order, mode):
+    """L7-L8 run the one-CTA anti-diagonal ring sweep in both exact modes:
+    bit-identical to the reference loop."""
+    osys, dsys = systems("poisson", k, 1e-6)
+    x0, f, r0 = inputs(osys, 6)
+    st = P.make_smoother(dsys, "lsgs", gs_mode=mode)
+    xd, rd = dev(x0), dev(r0)
+    for _ in range(2):
+        P.lsgs_sweep(st, xd, rd, order=order)
+    xo, ro = x0.copy(), r0.copy()
+    ost = O.OracleSmoother(osys, "lsgs")
+    for _ in range(2):
+        ost.lsgs(xo, ro, forward=(order == "forward"))
+    assert np.array_equal(host(xd), xo)
+    assert np.array_equal(host(rd), ro)
+
+
 @pytest.mark.parametrize("prob,k,alpha", CASES)
 def test_ne_gs_wavefront_mode(prob, k, alpha):
     """Reference order, delta-form arithmetic: 1e-12 (north_star bar)."""
