@@ -504,7 +504,7 @@ void level_ne_gs(const ocmg_level *lv, int mode, bool forward, double *x,
                                           cudaMemcpyDeviceToDevice, s));
         } else if (n1 <= kGsSmallMaxN1 && ((uintptr_t)x % 16 | (uintptr_t)r % 16) == 0) {
             // both exact modes: one CTA, levels separated by barriers
-            OCMG_LAUNCH(k_p1_gs_small, 1, kGsSmallThreads, gs_small_smem(n1), s, n1,
+            OCMG_LAUNCH(k_p1_gs_small, 1, 64 * ((n1 + 1) / 2 > 32 ? 2 : 1), gs_small_smem(n1), s, n1,
                         lv->tables.p, forward ? 1 : 0, x, r);
         } else if (n1 >= gsd::kMinN1 && n1 <= gsd::kMaxN1) {
             // both exact modes: one CTA, anti-diagonal ring of r

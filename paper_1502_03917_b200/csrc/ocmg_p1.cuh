@@ -209,7 +209,7 @@ __global__ void k_p1_gs_level(int n1, const double *__restrict__ T, int t,
 // level costs ~0.2 us (one dependent add chain + a division + a barrier)
 // where a launch per level, or the banded wavefront kernel, costs 0.7-1.7 us.
 constexpr int kGsSmallMaxN1 = 65;
-constexpr int kGsSmallThreads = 160;  // >= 2 * kGsSmallMaxN1
+constexpr int kGsSmallThreads = 128;  // 2 * 32 * ceil(((n1 + 1) / 2) / 32)
 inline size_t gs_small_smem(int n1) {
     return (4 * (size_t)n1 * n1 + kP1TableDoubles) * sizeof(double);
 }
@@ -226,31 +226,28 @@ __global__ void __launch_bounds__(kGsSmallThreads, 1)
     const int N = n1 * n1;
     double *sr = gs_sm, *sx = gs_sm + 2 * N, *sT = gs_sm + 4 * N;
     // 2N doubles per array: n1 odd => N odd, 2N even, 16-byte chunks
-    for (int i = 2 * threadIdx.x; i < 2 * N; i += 2 * kGsSmallThreads) {
+    for (int i = 2 * threadIdx.x; i < 2 * N; i += 2 * blockDim.x) {
         gs_cp16(sr + i, r + i);
         gs_cp16(sx + i, x + i);
     }
     static_assert(kP1TableDoubles % 2 == 0, "table size");
-    for (int i = 2 * threadIdx.x; i < kP1TableDoubles; i += 2 * kGsSmallThreads)
+    for (int i = 2 * threadIdx.x; i < kP1TableDoubles; i += 2 * blockDim.x)
         gs_cp16(sT + i, T + i);
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     const int depth = 3 * (n1 - 1) + 8;
-    const int k = threadIdx.x;
-    const int field = k >= n1 ? 1 : 0;
-    const int row = k - field * n1;
-    const bool active = k < 2 * n1;
+    // threads [0, P) take the leading field's unknowns of a level (diagonal
+    // ix + 2 iy = t in the sweep's own frame), [P, 2P) the trailing field's
+    // (t - 7), packed in row order so idle warps skip the level
+    const int P = blockDim.x / 2, k = threadIdx.x;
+    const bool lead = k < P;
+    const int idx = lead ? k : k - P;
+    const int field = lead == (forward != 0) ? 0 : 1;
     for (int t = 0; t < depth; ++t) {
-        int ix, iy;
-        if (forward) {
-            iy = row;
-            ix = (field ? t - 7 : t) - 2 * iy;
-        } else {
-            const int ixr = (field ? t : t - 7) - 2 * row;
-            ix = n1 - 1 - ixr;
-            iy = n1 - 1 - row;
-        }
-        if (active && ix >= 0 && ix < n1) {
+        const int lev = lead ? t : t - 7;
+        const int vy = (lev > n1 - 1 ? (lev - n1 + 2) / 2 : 0) + idx, vx = lev - 2 * vy;
+        const int ix = forward ? vx : n1 - 1 - vx, iy = forward ? vy : n1 - 1 - vy;
+        if (lev >= 0 && vx >= 0 && vy < n1) {
             const int c = 7 * p1_axis_class(iy, n1) + p1_axis_class(ix, n1);
             const int v = iy * n1 + ix;
             const bool l = ix > 0, rr = ix < n1 - 1, dn = iy > 0, up = iy < n1 - 1;
@@ -289,7 +286,7 @@ __global__ void __launch_bounds__(kGsSmallThreads, 1)
         }
         __syncthreads();
     }
-    for (int i = 2 * threadIdx.x; i < 2 * N; i += 2 * kGsSmallThreads) {
+    for (int i = 2 * threadIdx.x; i < 2 * N; i += 2 * blockDim.x) {
         *reinterpret_cast<double2 *>(r + i) = *reinterpret_cast<const double2 *>(sr + i);
         *reinterpret_cast<double2 *>(x + i) = *reinterpret_cast<const double2 *>(sx + i);
     }
