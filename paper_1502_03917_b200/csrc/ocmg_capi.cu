@@ -504,16 +504,26 @@ void level_ne_gs(const ocmg_level *lv, int mode, bool forward, double *x,
                                           cudaMemcpyDeviceToDevice, s));
         } else if (n1 <= kGsSmallMaxN1 && ((uintptr_t)x % 16 | (uintptr_t)r % 16) == 0) {
             // both exact modes: one CTA, levels separated by barriers
-            OCMG_LAUNCH(k_p1_gs_small, 1, 64 * ((n1 + 1) / 2 > 32 ? 2 : 1), gs_small_smem(n1), s, n1,
-                        lv->tables.p, forward ? 1 : 0, x, r);
+            const int nt = 64 * ((n1 + 1) / 2 > 32 ? 2 : 1);
+            if (mode == OCMG_GS_WAVEFRONT)
+                OCMG_LAUNCH(k_p1_gs_small<true>, 1, nt, gs_small_smem(n1), s, n1, lv->tables.p,
+                            forward ? 1 : 0, x, r);
+            else
+                OCMG_LAUNCH(k_p1_gs_small<false>, 1, nt, gs_small_smem(n1), s, n1, lv->tables.p,
+                            forward ? 1 : 0, x, r);
         } else if (n1 >= gsd::kMinN1 && n1 <= gsd::kMaxN1) {
             // both exact modes: one CTA, anti-diagonal ring of r
             const int nt = 2 * gsd::per_field(n1);
             const size_t sm = gsd::smem(n1);
-            if (forward)
-                OCMG_LAUNCH((k_p1_gs_diag<320, gsd::kRing, false>), 1, nt, sm, s, n1, lv->tables.p, x, r);
+            const bool fast = mode == OCMG_GS_WAVEFRONT;
+            if (forward && fast)
+                OCMG_LAUNCH((k_p1_gs_diag<320, gsd::kRing, false, true>), 1, nt, sm, s, n1, lv->tables.p, x, r);
+            else if (forward)
+                OCMG_LAUNCH((k_p1_gs_diag<320, gsd::kRing, false, false>), 1, nt, sm, s, n1, lv->tables.p, x, r);
+            else if (fast)
+                OCMG_LAUNCH((k_p1_gs_diag<320, gsd::kRing, true, true>), 1, nt, sm, s, n1, lv->tables.p, x, r);
             else
-                OCMG_LAUNCH((k_p1_gs_diag<320, gsd::kRing, true>), 1, nt, sm, s, n1, lv->tables.p, x, r);
+                OCMG_LAUNCH((k_p1_gs_diag<320, gsd::kRing, true, false>), 1, nt, sm, s, n1, lv->tables.p, x, r);
         } else if (mode == OCMG_GS_WAVEFRONT && lv->wf.ready()) {
             lv->wf.sweep(forward, x, r, s);
         } else {
@@ -1116,13 +1126,19 @@ int ocmg_level_create_p1(int k, double alpha, const double *tables,
             // per call: the attribute is per device, and cheap to set
             OCMG_CUDA(cudaFuncSetAttribute(k_p1_mc_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            mc_small_smem(kMcSmallMaxN1)));
-            OCMG_CUDA(cudaFuncSetAttribute(k_p1_gs_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            OCMG_CUDA(cudaFuncSetAttribute(k_p1_gs_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)gs_small_smem(kGsSmallMaxN1)));
+            OCMG_CUDA(cudaFuncSetAttribute(k_p1_gs_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)gs_small_smem(kGsSmallMaxN1)));
             {
                 const int gsm = (int)gsd::smem(gsd::kMaxN1);
-                OCMG_CUDA(cudaFuncSetAttribute(k_p1_gs_diag<320, gsd::kRing, false>,
+                OCMG_CUDA(cudaFuncSetAttribute(k_p1_gs_diag<320, gsd::kRing, false, false>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, gsm));
-                OCMG_CUDA(cudaFuncSetAttribute(k_p1_gs_diag<320, gsd::kRing, true>,
+                OCMG_CUDA(cudaFuncSetAttribute(k_p1_gs_diag<320, gsd::kRing, true, false>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, gsm));
+                OCMG_CUDA(cudaFuncSetAttribute(k_p1_gs_diag<320, gsd::kRing, false, true>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, gsm));
+                OCMG_CUDA(cudaFuncSetAttribute(k_p1_gs_diag<320, gsd::kRing, true, true>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, gsm));
             }
             lv->mc_tier = lv->n1 <= kMcSmallMaxN1 ? 0 : lv->n1 <= kMcGridMaxN1 ? 1 : 2;

@@ -202,12 +202,15 @@ __global__ void k_p1_gs_level(int n1, const double *__restrict__ T, int t,
 // The whole reference-order sweep of a small level in one CTA: x, r and the
 // class tables are staged in shared memory (cp.async), the 3(n1-1)+8
 // dependency levels are separated by __syncthreads instead of kernel
-// launches, and thread (field, row) owns the one unknown of its mesh row at
-// each level (the mapping of k_p1_gs_level).  Same arithmetic as
-// p1_gs_unknown, so bit-identical to the reference sweep; the scatter reuses
-// the gathered residual (no other unknown of the level touches it).  One
-// level costs ~0.2 us (one dependent add chain + a division + a barrier)
-// where a launch per level, or the banded wavefront kernel, costs 0.7-1.7 us.
+// launches, and the threads are packed onto each level's unknowns (the order
+// of k_p1_gs_level).  FAST = false: the arithmetic of p1_gs_unknown, so
+// bit-identical to the reference sweep (reference mode).  FAST = true (the
+// wavefront mode, checked at 1e-12): two FMA chains and a reciprocal
+// multiply, as in p1_mc_vertex, which shortens a level's dependent chain.
+// The scatter reuses the gathered residual (no other unknown of the level
+// touches it).  A level costs ~0.4 us (one warp's dependent chain and a
+// barrier) where a launch per level, or the banded wavefront kernel, costs
+// 0.7-1.7 us.
 constexpr int kGsSmallMaxN1 = 65;
 constexpr int kGsSmallThreads = 128;  // 2 * 32 * ceil(((n1 + 1) / 2) / 32)
 inline size_t gs_small_smem(int n1) {
@@ -219,6 +222,7 @@ __device__ __forceinline__ void gs_cp16(double *dst, const double *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
 }
 
+template <bool FAST>
 __global__ void __launch_bounds__(kGsSmallThreads, 1)
     k_p1_gs_small(int n1, const double *__restrict__ T, int forward,
                   double *__restrict__ x, double *__restrict__ r) {
@@ -262,12 +266,23 @@ __global__ void __launch_bounds__(kGsSmallThreads, 1)
             const double *W = sT + kP1OffW + c * 28 + 14 * field;
             const double *A = sT + kP1OffA + c * 28 + 14 * field;
             double s = 0.0;
+            if (FAST) {  // two FMA chains (the multicolour formula)
+                double s1 = 0.0;
 #pragma unroll
-            for (int d = 0; d < 7; ++d)
-                if (ex[d]) s = __dadd_rn(s, __dmul_rn(W[d], g[d]));
+                for (int d = 0; d < 7; ++d)
+                    if (ex[d]) {
+                        s = __fma_rn(W[d], g[d], s);
+                        s1 = __fma_rn(W[7 + d], g[7 + d], s1);
+                    }
+                s = __dadd_rn(s, s1);
+            } else {
 #pragma unroll
-            for (int d = 0; d < 7; ++d)
-                if (ex[d]) s = __dadd_rn(s, __dmul_rn(W[7 + d], g[7 + d]));
+                for (int d = 0; d < 7; ++d)
+                    if (ex[d]) s = __dadd_rn(s, __dmul_rn(W[d], g[d]));
+#pragma unroll
+                for (int d = 0; d < 7; ++d)
+                    if (ex[d]) s = __dadd_rn(s, __dmul_rn(W[7 + d], g[7 + d]));
+            }
             // every shared load before the first store (sr, sx and sT share
             // one array, so the compiler would not hoist them past a store)
             double a[14];
@@ -275,13 +290,15 @@ __global__ void __launch_bounds__(kGsSmallThreads, 1)
             for (int e = 0; e < 14; ++e) a[e] = A[e];
             const int i = field * N + v;
             const double xi = sx[i];
-            const double p = __ddiv_rn(s, sT[kP1OffND + c * 2 + field]);
+            const double nd = sT[kP1OffND + c * 2 + field];
+            const double p = FAST ? __dmul_rn(s, __drcp_rn(nd)) : __ddiv_rn(s, nd);
             sx[i] = __dadd_rn(xi, p);
 #pragma unroll
             for (int d = 0; d < 7; ++d)
                 if (ex[d]) {
-                    sr[nb[d]] = __dsub_rn(g[d], __dmul_rn(a[d], p));
-                    sr[N + nb[d]] = __dsub_rn(g[7 + d], __dmul_rn(a[7 + d], p));
+                    sr[nb[d]] = FAST ? __fma_rn(-a[d], p, g[d]) : __dsub_rn(g[d], __dmul_rn(a[d], p));
+                    sr[N + nb[d]] = FAST ? __fma_rn(-a[7 + d], p, g[7 + d])
+                                         : __dsub_rn(g[7 + d], __dmul_rn(a[7 + d], p));
                 }
         }
         __syncthreads();

@@ -18,7 +18,8 @@
 // swapped, so the kernel runs in virtual coordinates (vx, vy) = reflected
 // (ix, iy) and negates the stencil offsets; the arithmetic follows the real
 // CSR order d = 0..6 (p1_gs_unknown), so the result is bit-identical to the
-// reference sweep.
+// reference sweep (FAST = false); FAST = true is the wavefront mode's
+// arithmetic (two FMA chains, reciprocal multiply; 1e-12).
 #pragma once
 
 #include "ocmg_p1.cuh"
@@ -45,7 +46,7 @@ __device__ __forceinline__ void wait_group() {
 }
 }  // namespace gsd
 
-template <int MAXT, int R, bool BWD>
+template <int MAXT, int R, bool BWD, bool FAST>
 __global__ void __launch_bounds__(MAXT, 1)
     k_p1_gs_diag(int n1, const double *__restrict__ T, double *__restrict__ x,
                  double *__restrict__ r) {
@@ -121,22 +122,35 @@ __global__ void __launch_bounds__(MAXT, 1)
             const double *W = sT + kP1OffW + c * 28 + 14 * field;
             const double *A = sT + kP1OffA + c * 28 + 14 * field;
             double sum = 0.0;
+            if (FAST) {  // two FMA chains (the multicolour formula)
+                double s1 = 0.0;
 #pragma unroll
-            for (int d = 0; d < 7; ++d)
-                if (ex[d]) sum = __dadd_rn(sum, __dmul_rn(W[d], g[d]));
+                for (int d = 0; d < 7; ++d)
+                    if (ex[d]) {
+                        sum = __fma_rn(W[d], g[d], sum);
+                        s1 = __fma_rn(W[7 + d], g[7 + d], s1);
+                    }
+                sum = __dadd_rn(sum, s1);
+            } else {
 #pragma unroll
-            for (int d = 0; d < 7; ++d)
-                if (ex[d]) sum = __dadd_rn(sum, __dmul_rn(W[7 + d], g[7 + d]));
+                for (int d = 0; d < 7; ++d)
+                    if (ex[d]) sum = __dadd_rn(sum, __dmul_rn(W[d], g[d]));
+#pragma unroll
+                for (int d = 0; d < 7; ++d)
+                    if (ex[d]) sum = __dadd_rn(sum, __dmul_rn(W[7 + d], g[7 + d]));
+            }
             double a[14];  // before the first shared store (one array)
 #pragma unroll
             for (int e = 0; e < 14; ++e) a[e] = A[e];
-            const double p = __ddiv_rn(sum, sT[kP1OffND + c * 2 + field]);
+            const double nd = sT[kP1OffND + c * 2 + field];
+            const double p = FAST ? __dmul_rn(sum, __drcp_rn(nd)) : __ddiv_rn(sum, nd);
             x[field * N + iy * n1 + ix] = __dadd_rn(xi, p);
 #pragma unroll
             for (int d = 0; d < 7; ++d)
                 if (ex[d]) {
-                    ring[o[d]] = __dsub_rn(g[d], __dmul_rn(a[d], p));
-                    ring[o[d] + n1] = __dsub_rn(g[7 + d], __dmul_rn(a[7 + d], p));
+                    ring[o[d]] = FAST ? __fma_rn(-a[d], p, g[d]) : __dsub_rn(g[d], __dmul_rn(a[d], p));
+                    ring[o[d] + n1] = FAST ? __fma_rn(-a[7 + d], p, g[7 + d])
+                                           : __dsub_rn(g[7 + d], __dmul_rn(a[7 + d], p));
                 }
         }
         // the diagonal fetched at level t' is first read at level t'+R-15
