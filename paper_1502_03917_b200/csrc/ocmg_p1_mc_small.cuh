@@ -35,18 +35,25 @@ __global__ void __launch_bounds__(1024)
     const int N = n1 * n1;
     double2 *const xs = g + P * P;  // [n1^2] (state, adjoint)
     double *const Cs = reinterpret_cast<double *>(xs + N);  // [49][2][29]
+    // staging: every global read is an asynchronous copy, one wait for all
     for (int i = threadIdx.x; i < P * P; i += blockDim.x) {
         const int gy = i / P, gx = i - gy * P;
         const int ix = gx - 1, iy = gy - 1;
-        double2 v = make_double2(0.0, 0.0);
         if (ix >= 0 && ix < n1 && iy >= 0 && iy < n1) {
             const int k = iy * n1 + ix;
-            v = make_double2(r[k], r[N + k]);
+            mcs_cp8((unsigned)__cvta_generic_to_shared(&g[i].x), r + k, true);
+            mcs_cp8((unsigned)__cvta_generic_to_shared(&g[i].y), r + N + k, true);
+        } else {
+            g[i] = make_double2(0.0, 0.0);
         }
-        g[i] = v;
     }
-    for (int i = threadIdx.x; i < N; i += blockDim.x) xs[i] = make_double2(x[i], x[N + i]);
-    for (int i = threadIdx.x; i < 49 * 58; i += blockDim.x) Cs[i] = __ldg(C + i);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        mcs_cp8((unsigned)__cvta_generic_to_shared(&xs[i].x), x + i, true);
+        mcs_cp8((unsigned)__cvta_generic_to_shared(&xs[i].y), x + N + i, true);
+    }
+    for (int i = threadIdx.x; i < 49 * 58; i += blockDim.x)
+        mcs_cp8((unsigned)__cvta_generic_to_shared(Cs + i), C + i, true);
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     const int per_row = (n1 + 6) / 7;
     const int count = per_row * n1;
