@@ -1,68 +1,78 @@
-// Latency microbenchmarks (single warp, dependent chains), cycles per op.
-// nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o scripts/micro_lat scripts/micro_lat.cu
+// Dependent-chain latencies on one warp (dev tool): DFMA, DADD, DMUL,
+// IEEE DDIV (__ddiv_rn), DRCP+DMUL, LDS.64 pointer chase, BAR.SYNC with
+// 1..8 warps.  nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o scripts/micro_lat scripts/micro_lat.cu
 #include <cstdio>
 
-__global__ void k_lat(double *out, const double *g, long long *cyc, int n) {
-    __shared__ double sh[64];
-    const int lane = threadIdx.x;
-    sh[lane] = 1.0 + lane * 1e-3;
-    sh[lane + 32] = 1.0;
-    __syncwarp();
-    double a = out[lane], b = out[lane + 32], c = 1.0000001;
-    long long t0, t1;
-    // DFMA chain
-    t0 = clock64();
-    for (int i = 0; i < n; ++i) a = fma(a, c, b);
-    t1 = clock64();
-    cyc[0] = t1 - t0;
-    // DADD chain
-    t0 = clock64();
-    for (int i = 0; i < n; ++i) a = a + b;
-    t1 = clock64();
-    cyc[1] = t1 - t0;
-    // SHFL (double) chain
-    t0 = clock64();
-    for (int i = 0; i < n; ++i) a = __shfl_down_sync(0xffffffffu, a, 1) + 0.0;
-    t1 = clock64();
-    cyc[2] = t1 - t0;
-    // LDS chain (address depends on loaded value)
-    int idx = lane;
-    t0 = clock64();
-    for (int i = 0; i < n; ++i) idx = (int)sh[idx & 63] & 31;
-    t1 = clock64();
-    cyc[3] = t1 - t0;
-    // L2 (ld.cg) pointer chase over a 16 MB region
-    long long j = lane;
-    t0 = clock64();
-    for (int i = 0; i < n / 16; ++i) j = (long long)__ldcg(g + j);
-    t1 = clock64();
-    cyc[4] = (t1 - t0) * 16;
-    // __syncwarp cost
-    t0 = clock64();
-    for (int i = 0; i < n; ++i) __syncwarp();
-    t1 = clock64();
-    cyc[5] = t1 - t0;
-    out[lane] = a + (double)idx + (double)j;
+__global__ void k_lat(long long *out, double a, double b, int n) {
+    __shared__ long long sm_idx[1024];
+    __shared__ double sm_d[1024];
+    const int t = threadIdx.x;
+    for (int i = t; i < 1024; i += blockDim.x) {
+        sm_idx[i] = (i * 17 + 1) & 1023;
+        sm_d[i] = 1.0 + 1e-9 * i;
+    }
+    __syncthreads();
+    double x = a + t;
+    long long c0, c1;
+    // DFMA
+    c0 = clock64();
+    for (int i = 0; i < n; ++i) x = fma(x, b, a);
+    c1 = clock64();
+    if (t == 0) out[0] = c1 - c0;
+    // DADD
+    c0 = clock64();
+    for (int i = 0; i < n; ++i) x = x + b;
+    c1 = clock64();
+    if (t == 0) out[1] = c1 - c0;
+    // DMUL
+    c0 = clock64();
+    for (int i = 0; i < n; ++i) x = x * b;
+    c1 = clock64();
+    if (t == 0) out[2] = c1 - c0;
+    // DDIV
+    c0 = clock64();
+    for (int i = 0; i < n; ++i) x = __ddiv_rn(x, b);
+    c1 = clock64();
+    if (t == 0) out[3] = c1 - c0;
+    // rcp + mul
+    c0 = clock64();
+    for (int i = 0; i < n; ++i) x = x * __drcp_rn(b + x * 1e-300);
+    c1 = clock64();
+    if (t == 0) out[4] = c1 - c0;
+    // LDS chase
+    long long p = t & 1023;
+    c0 = clock64();
+    for (int i = 0; i < n; ++i) p = sm_idx[p];
+    c1 = clock64();
+    if (t == 0) out[5] = c1 - c0;
+    // LDS.64 double dependent (address from value)
+    double y = sm_d[t & 1023];
+    c0 = clock64();
+    for (int i = 0; i < n; ++i) y = sm_d[((long long)(y * 1e9)) & 1023];
+    c1 = clock64();
+    if (t == 0) out[6] = c1 - c0;
+    // barrier
+    __syncthreads();
+    c0 = clock64();
+    for (int i = 0; i < n; ++i) __syncthreads();
+    c1 = clock64();
+    if (t == 0) out[7] = c1 - c0;
+    if (x == 12345.0 || p == 99999 || y == 1.5) out[8] = 1;
 }
 
 int main() {
-    const int n = 4096;
-    double *out, *g;
-    long long *cyc;
-    cudaMalloc(&out, 64 * 8);
-    cudaMemset(out, 0, 64 * 8);
-    const size_t ng = 2 * 1024 * 1024;  // 16 MB
-    cudaMalloc(&g, ng * 8);
-    double *h = new double[ng];
-    for (size_t i = 0; i < ng; ++i) h[i] = (double)((i * 7919 + 4099) % ng);
-    cudaMemcpy(g, h, ng * 8, cudaMemcpyHostToDevice);
-    cudaMalloc(&cyc, 8 * 8);
-    k_lat<<<1, 32>>>(out, g, cyc, n);
-    k_lat<<<1, 32>>>(out, g, cyc, n);
-    cudaDeviceSynchronize();
-    long long c[8];
-    cudaMemcpy(c, cyc, 6 * 8, cudaMemcpyDeviceToHost);
-    const char *nm[] = {"DFMA", "DADD", "SHFL.f64+DADD", "LDS", "LDG.cg (L2)", "SYNCWARP"};
-    for (int i = 0; i < 6; ++i) printf("%-16s %6.1f cycles/op\n", nm[i], (double)c[i] / n);
+    long long *d, h[9];
+    cudaMalloc(&d, 9 * sizeof(long long));
+    const int n = 1000;
+    const char *names[8] = {"DFMA", "DADD", "DMUL", "DDIV (__ddiv_rn)", "DRCP+DMUL",
+                            "LDS.64 chase (int)", "LDS.64 chase (double)", "BAR.SYNC"};
+    for (int w : {1, 2, 4, 8}) {
+        for (int rep = 0; rep < 2; ++rep) k_lat<<<1, 32 * w>>>(d, 1.0000001, 0.9999999, n);
+        cudaDeviceSynchronize();
+        cudaMemcpy(h, d, 9 * sizeof(long long), cudaMemcpyDeviceToHost);
+        printf("warps=%d:", w);
+        for (int i = 0; i < 8; ++i) printf("  %s %.1f", names[i], (double)h[i] / n);
+        printf("\n");
+    }
     return 0;
 }

@@ -177,6 +177,24 @@ def test_ne_gs_wavefront_mode(prob, k, alpha):
     assert rel(host(rd), ro) < 1e-11
 
 
+@pytest.mark.parametrize("k,alpha", [(5, 1e-4), (6, 1e-6)])
+def test_stokes_wavefront_level_launches(k, alpha):
+    """Generic levels above the one-CTA size (a launch per dependency level,
+    a warp per row): 1e-12 against the reference loop, both directions."""
+    osys, dsys = systems("stokes", k, alpha)
+    x0, f, r0 = inputs(osys, 7)
+    st = P.make_smoother(dsys, "slsgs", gs_mode="wavefront")
+    xd, rd = dev(x0), dev(r0)
+    for _ in range(2):
+        st.sweep(xd, rd)
+    xo, ro = x0.copy(), r0.copy()
+    ost = O.OracleSmoother(osys, "slsgs")
+    for _ in range(2):
+        ost.sweep(xo, ro)
+    assert rel(host(xd), xo) < 1e-12
+    assert rel(host(rd), ro) < 1e-11
+
+
 @pytest.mark.parametrize("k", [7, 8, 10, 12])
 @pytest.mark.parametrize("order", ["forward", "backward"])
 def test_wavefront_vs_reference_mode_many_bands(k, order):
