@@ -375,9 +375,10 @@ void run_schedule(const ocmg_level *lv, const Schedule &S, bool reverse,
         if (warp_rows) {
             const int64_t thr = cnt * 32;
             const int blk = thr < 256 ? (int)thr : 256;
-            OCMG_LAUNCH(k_csr_gs_rows_warp, grid_for(thr, blk), blk, 0, s, (int)cnt,
-                        S.rows.p + lo, lv->A.off.p, lv->A.col.p, lv->A.val.p, lv->W.p,
-                        lv->ndiag.p, x, r);
+            OCMG_LAUNCH_PDL(k_csr_gs_rows_warp, grid_for(thr, blk), blk, 0, s, (int)cnt,
+                            (const int32_t *)(S.rows.p + lo), (const int64_t *)lv->A.off.p,
+                            (const int32_t *)lv->A.col.p, (const double *)lv->A.val.p,
+                            (const double *)lv->W.p, (const double *)lv->ndiag.p, x, r);
         } else if (S.has_gsell) {
             const int64_t s0 = S.gslice[l], slots = (S.gslice[l + 1] - s0) * 32;
             const int blk = slots < 128 ? (int)slots : 128;

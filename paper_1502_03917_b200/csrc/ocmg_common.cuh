@@ -48,6 +48,32 @@ inline std::atomic<long long> &launch_counter() {
         kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);          \
     } while (0)
 
+// The same with programmatic dependent launch: the grid may be scheduled
+// while the previous kernel on the stream is still running; the kernel must
+// execute griddepcontrol.wait (pdl_wait) before touching what that kernel
+// writes.  Used for chains of short dependent launches (one per dependency
+// level), where it hides the launch latency behind the previous level.
+#define OCMG_LAUNCH_PDL(kernel, grid, block, smem, strm_, ...)                \
+    do {                                                                     \
+        ::ocmg::launch_counter().fetch_add(1, std::memory_order_relaxed);    \
+        cudaLaunchConfig_t cfg_{};                                           \
+        cfg_.gridDim = dim3(grid);                                           \
+        cfg_.blockDim = dim3(block);                                         \
+        cfg_.dynamicSmemBytes = (smem);                                      \
+        cfg_.stream = (strm_);                                               \
+        cudaLaunchAttribute at_[1];                                          \
+        at_[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;      \
+        at_[0].val.programmaticStreamSerializationAllowed = 1;               \
+        cfg_.attrs = at_;                                                    \
+        cfg_.numAttrs = 1;                                                   \
+        OCMG_CUDA(cudaLaunchKernelEx(&cfg_, kernel, __VA_ARGS__));           \
+    } while (0)
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Owning device allocation (cudaMalloc/cudaFree).
 template <class T>
 struct DevBuf {

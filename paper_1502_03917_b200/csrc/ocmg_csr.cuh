@@ -257,9 +257,12 @@ __global__ void k_csr_gs_rows_warp(int cnt, const int32_t *__restrict__ rows,
                                    double *__restrict__ x, double *__restrict__ r) {
     const int wid = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
+    pdl_trigger();  // the next level may start launching now
     if (wid >= cnt) return;
+    // the row's structure does not depend on the previous level; r and x do
     const int32_t i = rows[wid];
     const int64_t b = off[i], e = off[i + 1];
+    pdl_wait();
     double q = 0.0;
     for (int64_t t = b + lane; t < e; t += 32) q = fma(w[t], r[col[t]], q);
 #pragma unroll
