@@ -410,6 +410,8 @@ __global__ void k_vanka_level(int cnt, const int32_t *__restrict__ ids,
                               const int32_t *__restrict__ acol,
                               const double *__restrict__ aval, double tau,
                               double *__restrict__ x, double *__restrict__ r) {
+    pdl_trigger();  // launched with PDL in the per-level loops
+    pdl_wait();
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (w >= cnt) return;
     const int p = ids[w];
@@ -447,7 +449,7 @@ void level_vanka(const ocmg_level *lv, double tau, bool forward, double *x, doub
         if (!cnt) continue;
         const int64_t thr = cnt * 32;
         const int blk = thr < 128 ? (int)thr : 128;
-        OCMG_LAUNCH(k_vanka_level, grid_for(thr, blk), blk, 0, s, (int)cnt, S.rows.p + lo,
+        OCMG_LAUNCH_PDL(k_vanka_level, grid_for(thr, blk), blk, 0, s, (int)cnt, S.rows.p + lo,
                     lv->vk_off.p, lv->vk_dofs.p, lv->vk_inv.p, lv->vk_mmax, lv->A.off.p,
                     lv->A.col.p, lv->A.val.p, tau, x, r);
     }
@@ -531,7 +533,7 @@ void level_ne_gs(const ocmg_level *lv, int mode, bool forward, double *x,
             const int depth = 3 * (n1 - 1) + 8;
             const int blk = 2 * n1 < 256 ? 32 * ((2 * n1 + 31) / 32) : 256;
             for (int t = 0; t < depth; ++t)
-                OCMG_LAUNCH(k_p1_gs_level, grid_for(2 * n1, blk), blk, 0, s, 
+                OCMG_LAUNCH_PDL(k_p1_gs_level, grid_for(2 * n1, blk), blk, 0, s, 
                     n1, lv->tables.p, t, forward ? 1 : 0, x, r);
         }
         OCMG_LAUNCH_CHECK();
@@ -595,10 +597,10 @@ void level_cgs(const ocmg_level *lv, int mode, double *x, double *r, double *scr
     } else {
         const int blk = n1 < 256 ? 32 * ((n1 + 31) / 32) : 256;
         for (int l = 0; l <= 2 * (n1 - 1); ++l) {
-            OCMG_LAUNCH(k_p1_cgs_solve, grid_for(n1, blk), blk, 0, s, n1, lv->tables.p,
-                        lv->alpha, 0, l, x, r, scratch);
-            OCMG_LAUNCH(k_p1_cgs_apply, grid_for(5 * (int64_t)n1, kBlk), kBlk, 0, s, n1,
-                        lv->tables.p, 0, l, scratch, r);
+            OCMG_LAUNCH_PDL(k_p1_cgs_solve, grid_for(n1, blk), blk, 0, s, n1, lv->tables.p,
+                            lv->alpha, 0, l, x, r, scratch);
+            OCMG_LAUNCH_PDL(k_p1_cgs_apply, grid_for(5 * (int64_t)n1, kBlk), kBlk, 0, s, n1,
+                            lv->tables.p, 0, l, scratch, r);
         }
     }
     OCMG_LAUNCH_CHECK();

@@ -35,6 +35,8 @@ __device__ __forceinline__ bool cgs_sel(int ix, int iy, int sel_mod, int sel) {
 __global__ void k_p1_cgs_solve(int n1, const double *__restrict__ T, double alpha,
                                int sel_mod, int sel, double *__restrict__ x,
                                const double *__restrict__ r, double *__restrict__ S) {
+    pdl_trigger();  // launched with PDL in the per-level loops
+    pdl_wait();
     const int64_t N = (int64_t)n1 * n1;
     int ix, iy;
     if (sel_mod) {  // colour: thread per vertex of the colour in row iy
@@ -71,6 +73,8 @@ __global__ void k_p1_cgs_solve(int n1, const double *__restrict__ T, double alph
 __global__ void k_p1_cgs_apply(int n1, const double *__restrict__ T, int sel_mod,
                                int sel, const double *__restrict__ S,
                                double *__restrict__ r) {
+    pdl_trigger();  // launched with PDL in the per-level loops
+    pdl_wait();
     const int64_t N = (int64_t)n1 * n1;
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     int ix, iy;

@@ -179,6 +179,8 @@ __device__ __forceinline__ void p1_gs_unknown(int field, int ix, int iy,
 __global__ void k_p1_gs_level(int n1, const double *__restrict__ T, int t,
                               int forward, double *__restrict__ x,
                               double *__restrict__ r) {
+    pdl_trigger();  // launched with PDL in the per-level loops
+    pdl_wait();
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= 2 * n1) return;
     const int field = k >= n1 ? 1 : 0;
