@@ -308,7 +308,7 @@ void level_residual(const ocmg_level *lv, const double *x, const double *f,
         if (yhi < 0) yhi = lv->n1;
         if (lv->n1 <= kSmallN1 && ylo == 0 && yhi == lv->n1) {
             const int64_t N = (int64_t)lv->n1 * lv->n1;
-            OCMG_LAUNCH(k_p1_residual_all, grid_for(N, kBlk), kBlk, 0, s, lv->n1,
+            OCMG_LAUNCH_PDL(k_p1_residual_all, grid_for(N, kBlk), kBlk, 0, s, lv->n1,
                         lv->tables.p, x, f, r);
             OCMG_LAUNCH_CHECK();
             return;
@@ -461,7 +461,7 @@ void level_vanka(const ocmg_level *lv, double tau, bool forward, double *x, doub
 bool p1_mc_sweep(const ocmg_level *lv, bool forward, double *x, double *r,
                  double *rout, cudaStream_t s) {
     if (lv->mc_tier == 0) {
-        OCMG_LAUNCH(k_p1_mc_small, 1, 1024, mc_small_smem(lv->n1), s, lv->n1,
+        OCMG_LAUNCH_PDL(k_p1_mc_small, 1, 1024, mc_small_smem(lv->n1), s, lv->n1,
                     forward ? 1 : 0, lv->mc_coef.p, x, r);
         OCMG_LAUNCH_CHECK();
         return false;
@@ -712,6 +712,8 @@ __global__ void __launch_bounds__(256)
     k_coarse_inv(int n, const double *__restrict__ inv, int stokes, int p_off,
                  int mu_off, int n_p, const double *__restrict__ rhs,
                  double *__restrict__ xout) {
+    pdl_trigger();  // launched with PDL (short dependent launches of a cycle)
+    pdl_wait();
     extern __shared__ double b[];
     __shared__ double sh[32];
     __shared__ double mean[2];
@@ -767,7 +769,7 @@ void coarse_solve_inv(const ocmg_coarse *c, const double *rhs, double *x,
     const int n = (int)c->n;
     const size_t smem = (size_t)n * sizeof(double);
     const bool stokes = c->problem == OCMG_STOKES;
-    OCMG_LAUNCH(k_coarse_inv, (n + 7) / 8, 256, smem, s, n, c->inv.p, stokes ? 1 : 0,
+    OCMG_LAUNCH_PDL(k_coarse_inv, (n + 7) / 8, 256, smem, s, n, c->inv.p, stokes ? 1 : 0,
                 (int)c->p_off, (int)c->mu_off, (int)c->n_p, rhs, x);
     if (stokes)
         OCMG_LAUNCH(k_coarse_recentre, 1, 256, 0, s, (int)c->p_off, (int)c->mu_off,
@@ -795,11 +797,11 @@ void do_restrict(const ocmg_transfer *t, const double *rf, double *rc,
         if (rows <= 0) return;
         if (m <= kSmallN1) {  // small level: a coarse row per thread
             const dim3 g((m + kTX - 1) / kTX, (rows + kTY - 1) / kTY);
-            OCMG_LAUNCH(k_p1_restrict_tiled<1>, g, dim3(kTX, kTY), 0, s, t->nc1,
+            OCMG_LAUNCH_PDL(k_p1_restrict_tiled<1>, g, dim3(kTX, kTY), 0, s, t->nc1,
                         t->n_fields, rf, rc, cylo, cyhi);
         } else {
             const dim3 g((m + kTX - 1) / kTX, (rows + kTY * kRPT - 1) / (kTY * kRPT));
-            OCMG_LAUNCH(k_p1_restrict_tiled<kRPT>, g, dim3(kTX, kTY), 0, s, t->nc1,
+            OCMG_LAUNCH_PDL(k_p1_restrict_tiled<kRPT>, g, dim3(kTX, kTY), 0, s, t->nc1,
                         t->n_fields, rf, rc, cylo, cyhi);
         }
     } else {
@@ -819,15 +821,15 @@ void do_prolong_add(const ocmg_transfer *t, const double *c, double *xf,
         const bool all = fylo == 0 && fyhi == nf1;
         if (nf1 <= kSmallN1 && all) {  // small level: a coarse row per thread
             const dim3 g((nf1 + kTX - 1) / kTX, (crows + kTY - 1) / kTY);
-            OCMG_LAUNCH((k_p1_prolong_add_tiled<true, 1>), g, dim3(kTX, kTY), 0, s, t->nc1,
+            OCMG_LAUNCH_PDL((k_p1_prolong_add_tiled<true, 1>), g, dim3(kTX, kTY), 0, s, t->nc1,
                         t->n_fields, c, xf, fylo, fyhi);
         } else {
             const dim3 g((nf1 + kTX - 1) / kTX, (crows + kTY * kPRPT - 1) / (kTY * kPRPT));
             if (all)
-                OCMG_LAUNCH((k_p1_prolong_add_tiled<true, kPRPT>), g, dim3(kTX, kTY), 0, s,
+                OCMG_LAUNCH_PDL((k_p1_prolong_add_tiled<true, kPRPT>), g, dim3(kTX, kTY), 0, s,
                             t->nc1, t->n_fields, c, xf, fylo, fyhi);
             else
-                OCMG_LAUNCH((k_p1_prolong_add_tiled<false, kPRPT>), g, dim3(kTX, kTY), 0, s,
+                OCMG_LAUNCH_PDL((k_p1_prolong_add_tiled<false, kPRPT>), g, dim3(kTX, kTY), 0, s,
                             t->nc1, t->n_fields, c, xf, fylo, fyhi);
         }
     } else {
@@ -892,7 +894,7 @@ void cycle_rec(ocmg_hierarchy *h, int hi, double *x, const double *rhs,
         SubcycleParams P = h->sub;
         P.x = x;
         P.rhs = rhs;
-        OCMG_LAUNCH(k_p1_subcycle, 1, kSubThreads, h->sub_smem, s, P);
+        OCMG_LAUNCH_PDL(k_p1_subcycle, 1, kSubThreads, h->sub_smem, s, P);
         OCMG_LAUNCH_CHECK();
         return;
     }

@@ -30,6 +30,8 @@ __host__ __device__ constexpr int mc_small_smem(int n1) {
 __global__ void __launch_bounds__(1024)
     k_p1_mc_small(int n1, int forward, const double *__restrict__ C,
                   double *__restrict__ x, double *__restrict__ r) {
+    pdl_trigger();  // launched with PDL (short dependent launches of a cycle)
+    pdl_wait();
     extern __shared__ double2 g[];  // [(n1+2)^2] (state, adjoint), zero guards
     const int P = n1 + 2;
     const int N = n1 * n1;

@@ -165,6 +165,8 @@ __global__ void k_p1_residual_all(int n1, const double *__restrict__ T,
                                   const double *__restrict__ x,
                                   const double *__restrict__ f,
                                   double *__restrict__ r) {
+    pdl_trigger();  // launched with PDL (short dependent launches of a cycle)
+    pdl_wait();
     const int64_t N = (int64_t)n1 * n1;
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= N) return;
@@ -360,6 +362,8 @@ template <int RPT>  // coarse rows per thread (kRPT; 1 on small levels)
 __global__ void __launch_bounds__(kTX *kTY)
     k_p1_restrict_tiled(int nc1, int n_fields, const double *__restrict__ rf,
                         double *__restrict__ rc, int cylo, int cyhi) {
+    pdl_trigger();  // launched with PDL (short dependent launches of a cycle)
+    pdl_wait();
     // coarse rows [cylo, cyhi)
     const int cx = blockIdx.x * kTX + threadIdx.x;
     const int cy0 = cylo + (blockIdx.y * kTY + threadIdx.y) * RPT;
@@ -415,6 +419,8 @@ template <bool ALL, int PR>  // ALL: the whole level (no row-range guards); PR c
 __global__ void __launch_bounds__(kTX *kTY, 3)
     k_p1_prolong_add_tiled(int nc1, int n_fields, const double *__restrict__ c,
                            double *__restrict__ xf, int fylo, int fyhi) {
+    pdl_trigger();  // launched with PDL (short dependent launches of a cycle)
+    pdl_wait();
     // fine rows [fylo, fyhi), walked as coarse rows [fylo/2, (fyhi+1)/2)
     const int nf1 = 2 * nc1 - 1;
     const int fx = blockIdx.x * kTX + threadIdx.x;

@@ -216,6 +216,8 @@ __device__ __forceinline__ void coarse(int n, const double *__restrict__ inv, co
 
 __global__ void __launch_bounds__(kSubThreads, 1)
     k_p1_subcycle(const __grid_constant__ SubcycleParams P) {
+    pdl_trigger();  // launched with PDL (short dependent launches of a cycle)
+    pdl_wait();
     extern __shared__ double sm[];
     int n1s[kSubMaxK];
     for (int j = 0; j < P.nlev; ++j) n1s[j] = P.lv[j].n1;
