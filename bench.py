@@ -566,11 +566,22 @@ def run_gpu_arm(args, ws, rank, local):
                       "xd": torch.empty_like(x), "ri": torch.empty_like(r),
                       "ro": torch.empty_like(r), "s": torch.cuda.Stream()})
 
+    # a level's device scratch (wavefront flags and rings, multicolour
+    # barriers) belongs to one stream at a time (include/ocmg_b200.h), so the
+    # sweeps themselves are ordered across the two streams by an event; only
+    # the copies overlap
+    swept = [None]
+
     def e2e_job(sl):
         with torch.cuda.stream(sl["s"]):
             sl["xd"].copy_(sl["xh"], non_blocking=True)
             sl["ri"].copy_(sl["rh"], non_blocking=True)
+            if swept[0] is not None:
+                sl["s"].wait_event(swept[0])
             lsgs_sweep_into(st, sl["xd"], sl["ri"], sl["ro"])
+            ev = torch.cuda.Event()
+            ev.record(sl["s"])
+            swept[0] = ev
             sl["xh"].copy_(sl["xd"], non_blocking=True)
             sl["rh"].copy_(sl["ro"], non_blocking=True)
 
@@ -579,6 +590,7 @@ def run_gpu_arm(args, ws, rank, local):
         ev1 = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         ev0.record(stream)
+        swept[0] = None
         for sl in slots:
             sl["s"].wait_event(ev0)
         for i in range(k):

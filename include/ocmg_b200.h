@@ -18,7 +18,11 @@
  *     assembly.py:205-226), so x / r / f tensors are interchangeable with the
  *     reference's numpy arrays after a host<->device copy;
  *   - calls are stream-ordered and asynchronous unless stated; a handle may
- *     be used by one stream at a time (SURVEY.md §8(b) threading row);
+ *     be used by one stream at a time (SURVEY.md §8(b) threading row): a
+ *     level owns device scratch (the exact-order sweep's progress flags and
+ *     ring buffers, multicolour barriers, reduction partials), so two
+ *     sweeps of the same level on different streams must be ordered by the
+ *     caller with events, or they corrupt each other's scratch;
  *   - status: 0 ok; OCMG_E_ARG (-> ValueError), OCMG_E_CUDA
  *     (-> RuntimeError), OCMG_E_SINGULAR (-> SingularMatrixError,
  *     sparse.py:18-19); ocmg_last_error() returns the message of the last
@@ -253,6 +257,14 @@ int ocmg_cycle(ocmg_hierarchy *h, double *x, const double *f, void *stream);
 int ocmg_solve(ocmg_hierarchy *h, double *x, const double *f, double tol,
                int max_cycles, int use_graph, double *hist, int *n_done,
                void *stream);
+/* ocmg_solve with the reference's divergence stop made explicit
+ * (multigrid.py:26 DIVERGENCE_FACTOR = 1e6, multigrid.py:198-200): the loop
+ * also ends, with *diverged = 1, once rel > divergence_factor * rel0 (rel0 =
+ * the entering iterate's relative residual) or rel is not finite.
+ * divergence_factor <= 0 disables the test.  ocmg_solve = this with 1e6. */
+int ocmg_solve_ex(ocmg_hierarchy *h, double *x, const double *f, double tol,
+                  int max_cycles, int use_graph, double divergence_factor,
+                  double *hist, int *n_done, int *diverged, void *stream);
 
 #ifdef __cplusplus
 }

@@ -93,6 +93,8 @@ SIGNATURES = {
     "ocmg_cycle": (_I, [_P, _P, _P, _P]),
     "ocmg_solve": (_I, [_P, _P, _P, _D, _I, _I, _P, ctypes.POINTER(_I),
                         _P]),
+    "ocmg_solve_ex": (_I, [_P, _P, _P, _D, _I, _I, _D, _P,
+                           ctypes.POINTER(_I), ctypes.POINTER(_I), _P]),
 }
 
 

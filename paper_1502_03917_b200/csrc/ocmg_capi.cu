@@ -1610,8 +1610,18 @@ int ocmg_cycle(ocmg_hierarchy *h, double *x, const double *f, void *stream) {
 int ocmg_solve(ocmg_hierarchy *h, double *x, const double *f, double tol,
                int max_cycles, int use_graph, double *hist, int *n_done,
                void *stream) {
+    int diverged = 0;
+    return ocmg_solve_ex(h, x, f, tol, max_cycles, use_graph, 1e6, hist,
+                         n_done, &diverged, stream);
+}
+
+int ocmg_solve_ex(ocmg_hierarchy *h, double *x, const double *f, double tol,
+                  int max_cycles, int use_graph, double divergence_factor,
+                  double *hist, int *n_done, int *diverged, void *stream) {
     return guarded([&] {
-        OCMG_REQUIRE(h && x && f && hist && n_done, "null argument");
+        OCMG_REQUIRE(h && x && f && hist && n_done && diverged,
+                     "null argument");
+        *diverged = 0;
         cudaStream_t s = as_stream(stream);
         if (use_graph && s == nullptr) {
             // the legacy default stream cannot be captured: run the solve on
@@ -1633,6 +1643,16 @@ int ocmg_solve(ocmg_hierarchy *h, double *x, const double *f, double tol,
         OCMG_CUDA(cudaStreamSynchronize(s));
         const double fn = std::sqrt(fn2);
         OCMG_REQUIRE(fn > 0.0, "right-hand side is zero");
+        // relative residual of the entering iterate: the divergence test's
+        // norm0 (multigrid.py:26,198-200 abort once the norm exceeds
+        // DIVERGENCE_FACTOR * norm0)
+        level_residual(fine, x, f, h->tmp.p, s);
+        sumsq(fine->n, h->tmp.p, nullptr, fine->partial.p, h->scal.p + 2, s);
+        double r02 = 0.0;
+        OCMG_CUDA(cudaMemcpyAsync(&r02, h->scal.p + 2, sizeof(double),
+                                  cudaMemcpyDeviceToHost, s));
+        OCMG_CUDA(cudaStreamSynchronize(s));
+        const double rel0 = std::sqrt(r02) / fn;
         const bool graphs = use_graph && s != nullptr;
         if (graphs && (h->graph_x != x || h->graph_f != f ||
                        h->graph_stream != s)) {
@@ -1666,7 +1686,12 @@ int ocmg_solve(ocmg_hierarchy *h, double *x, const double *f, double tol,
             const double rel = std::sqrt(r2) / fn;
             hist[c] = rel;
             done = c + 1;
-            if (rel <= tol || !std::isfinite(rel)) break;
+            if (rel <= tol) break;
+            if (!std::isfinite(rel) ||
+                (divergence_factor > 0.0 && rel > divergence_factor * rel0)) {
+                *diverged = 1;
+                break;
+            }
         }
         *n_done = done;
     });

@@ -222,7 +222,9 @@ class Multigrid:
         """BASELINE.json protocol: x0 = 0 (or ``x``), repeat
         {cycle; mean projection; rel = ||f-Ax||_2/||f||_2} until rel <= tol.
         Runs entirely on the device (one graph replay + one scalar read per
-        cycle).  Returns (x, rel_history)."""
+        cycle).  Returns (x, rel_history).  Like ``solve`` it stops once
+        rel exceeds DIVERGENCE_FACTOR times the entering relative residual
+        (multigrid.py:26,198-200); ``self.last_diverged`` records it."""
         system = self.finest
         fd, _ = as_device(f, system.n)
         fresh = x is None
@@ -235,11 +237,13 @@ class Multigrid:
             x.zero_()
         xd, xnp = as_device(x, system.n)
         hist = np.zeros(max_cycles)
-        done = ctypes.c_int()
-        _lib.call("ocmg_solve", self.native().handle, _lib.dptr(xd),
+        done, div = ctypes.c_int(), ctypes.c_int()
+        _lib.call("ocmg_solve_ex", self.native().handle, _lib.dptr(xd),
                   _lib.dptr(fd), float(tol), int(max_cycles),
-                  1 if use_graph else 0, _lib.hptr(hist), ctypes.byref(done),
+                  1 if use_graph else 0, float(DIVERGENCE_FACTOR),
+                  _lib.hptr(hist), ctypes.byref(done), ctypes.byref(div),
                   _lib.stream_ptr())
+        self.last_diverged = bool(div.value)
         back_inplace(xd, x, xnp)
         if fresh:
             x = x.clone()

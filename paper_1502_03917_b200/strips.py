@@ -95,17 +95,20 @@ def exchange_ghosts(slab, part, group=None):
     import torch.distributed as dist
     if part.world_size == 1:
         return
-    sends, recvs = [], []
+    # one grouped batch (ncclGroupStart/End under NCCL): both neighbours
+    # send first, which ungrouped NCCL point-to-point calls may deadlock on
+    ops, recvs = [], []
     for peer, (a, b), (c, d) in ghost_plan(part):
         sbuf = slab[:, a:b].contiguous()
         rbuf = torch.empty_like(slab[:, c:d])
-        sends.append(dist.isend(sbuf, peer, group=group))
-        recvs.append((dist.irecv(rbuf, peer, group=group), rbuf, c, d))
-    for req, rbuf, c, d in recvs:
-        req.wait()
+        ops.append(dist.P2POp(dist.isend, sbuf, peer, group=group))
+        ops.append(dist.P2POp(dist.irecv, rbuf, peer, group=group))
+        recvs.append((rbuf, c, d))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    for rbuf, c, d in recvs:
         slab[:, c:d].copy_(rbuf)
-    for req in sends:
-        req.wait()
 
 
 class LoopbackExchange:
@@ -248,17 +251,19 @@ class DistComm:
         y0, y1 = st.bounds[level]
         n1 = st.n1[level]
         v = getattr(st, name)[level]
-        reqs = []
+        ops = []
         for peer in (st.rank - 1, st.rank + 1):
             if not 0 <= peer < st.world_size:
                 continue
             snd = (y0, y0 + g) if peer < st.rank else (y1 - g, y1)
             rcv = (y0 - g, y0) if peer < st.rank else (y1, y1 + g)
             for s_f, r_f in zip(_rows(v, n1, *snd), _rows(v, n1, *rcv)):
-                reqs.append(dist.isend(s_f, peer, group=self.group))
-                reqs.append(dist.irecv(r_f, peer, group=self.group))
-        for r in reqs:
-            r.wait()
+                ops.append(dist.P2POp(dist.isend, s_f, peer, group=self.group))
+                ops.append(dist.P2POp(dist.irecv, r_f, peer, group=self.group))
+        # grouped (ncclGroupStart/End): both neighbours post sends first
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
 
     def allgather(self, states, level, name):
         import torch.distributed as dist
