@@ -1700,21 +1700,8 @@ int ocmg_solve_ex(ocmg_hierarchy *h, double *x, const double *f, double tol,
 }  // extern "C"
 
 // ---------------------------------------------------------------------------
-// internal debug hook (not part of the ABI in include/ocmg_b200.h): copies a
-// wavefront ring buffer (0: chain-1 p, 1: chain-2 p, 2: u) to `out` (device)
+// internal debug hooks (not part of the ABI in include/ocmg_b200.h)
 // ---------------------------------------------------------------------------
-extern "C" int ocmg__debug_wf_ring(const ocmg_level *lv, int which, double *out,
-                                   int64_t *count) {
-    return guarded([&] {
-        OCMG_REQUIRE(lv && lv->kind == kP1 && lv->wf.ready(), "no wavefront");
-        const DevBuf<double> &src =
-            which == 0 ? lv->wf.ring1 : which == 1 ? lv->wf.ring2 : lv->wf.ringu;
-        *count = (int64_t)src.n;
-        if (out)
-            OCMG_CUDA(cudaMemcpy(out, src.p, src.n * sizeof(double),
-                                 cudaMemcpyDeviceToDevice));
-    });
-}
 
 // internal: per-warp iteration timestamps of the last wavefront sweep
 // (only when built with -DOCMG_WF_PROFILE); returns nb, niter, nwarps
@@ -1723,7 +1710,7 @@ extern "C" int ocmg__debug_wf_prof(const ocmg_level *lv, unsigned long long *out
     return guarded([&] {
         OCMG_REQUIRE(lv && lv->kind == kP1 && lv->wf.ready(), "no wavefront");
         dims[0] = lv->wf.nb;
-        dims[1] = lv->wf.niter;
+        dims[1] = lv->wf.niter();
         dims[2] = wf::NWARPS;
         dims[3] = (int64_t)lv->wf.prof.n;
         if (out && lv->wf.prof.n)
