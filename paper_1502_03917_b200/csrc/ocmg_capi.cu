@@ -361,7 +361,17 @@ void run_schedule(const ocmg_level *lv, const Schedule &S, bool reverse,
                   double *x, double *r, cudaStream_t s, bool warp_rows = false) {
     const int64_t nb = (int64_t)S.off.size() - 1;
     if (lv->n <= kCsrSmallN) {
-        // small level: every group in one CTA, __syncthreads between groups
+        // small level: every group in one CTA, __syncthreads between groups;
+        // staged in shared memory when it fits
+        const size_t sm = csr_small_smem(lv->n, lv->A.nnz, nb);
+        if (sm <= kCsrSmallSmemMax) {
+            const int nt = lv->n < 1024 ? (int)(32 * ((lv->n + 31) / 32)) : 1024;
+            OCMG_LAUNCH(k_csr_gs_sched_smem, 1, nt, sm, s, (int)nb, S.doff.p, S.rows.p,
+                        reverse ? 1 : 0, (int)lv->n, lv->A.off.p, lv->A.col.p, lv->A.val.p,
+                        lv->W.p, lv->ndiag.p, x, r);
+            OCMG_LAUNCH_CHECK();
+            return;
+        }
         OCMG_LAUNCH(k_csr_gs_sched_small, 1, 1024, 0, s, (int)nb, S.doff.p,
                     S.rows.p, reverse ? 1 : 0, lv->A.off.p, lv->A.col.p, lv->A.val.p,
                     lv->W.p, lv->ndiag.p, x, r);
@@ -934,14 +944,22 @@ void setup_subcycle(ocmg_hierarchy *h) {
         return;
     if (!h->coarse->inv.p || h->coarse->problem != OCMG_POISSON) return;
     const ocmg_level *l0 = h->levels[0];
-    if (l0->kind != kP1 || l0->k - 1 < 3) return;
-    const int nc1 = (1 << (l0->k - 1)) + 1;
+    // a generic bottom level: Poisson L2 (n1 = 5, too small for the 49
+    // class tables) over the reference's default coarsest level L1
+    auto csr_l2 = [](const ocmg_level *lv) {
+        return lv->kind != kP1 && lv->problem == OCMG_POISSON && lv->n == 50 &&
+               lv->has_colours && lv->A.nnz <= kSubCsrNnz &&
+               (int64_t)lv->colours.off.size() <= kSubCsrRows && lv->n < kSubCsrRows;
+    };
+    if (l0->kind != kP1 && !csr_l2(l0)) return;
+    const int nc1 = l0->kind == kP1 ? (1 << (l0->k - 1)) + 1 : 3;
     if (h->coarse->n != 2 * (int64_t)nc1 * nc1) return;
-    int top = 0;  // last hierarchy index with a structured level k <= kSubMaxK
+    int top = 0;  // last hierarchy index with a level k <= kSubMaxK
     for (int hi = 1; hi <= (int)h->levels.size(); ++hi) {
         const ocmg_level *lv = h->levels[hi - 1];
         const ocmg_transfer *t = h->transfers[hi - 1];
-        if (lv->kind != kP1 || lv->k > kSubMaxK || t->kind != kP1) break;
+        const bool ok = lv->kind == kP1 ? lv->k <= kSubMaxK : (hi == 1 && csr_l2(lv));
+        if (!ok || t->kind != kP1) break;
         top = hi;
     }
     if (top < 1 || top + 1 > kSubMaxK) return;
@@ -956,8 +974,24 @@ void setup_subcycle(ocmg_hierarchy *h) {
     int n1s[kSubMaxK] = {nc1};
     for (int j = 1; j <= top; ++j) {
         const ocmg_level *lv = h->levels[j - 1];
-        P.lv[j] = SubLevel{lv->n1, lv->tables.p, lv->mc_coef.p};
-        n1s[j] = lv->n1;
+        SubLevel &sl = P.lv[j];
+        if (lv->kind == kP1) {
+            sl.n1 = lv->n1;
+            sl.T = lv->tables.p;
+            sl.C = lv->mc_coef.p;
+        } else {
+            sl.n1 = 5;
+            sl.csr = 1;
+            sl.ngroups = (int)lv->colours.off.size() - 1;
+            sl.off = lv->A.off.p;
+            sl.col = lv->A.col.p;
+            sl.val = lv->A.val.p;
+            sl.w = lv->W.p;
+            sl.nd = lv->ndiag.p;
+            sl.goff = lv->colours.doff.p;
+            sl.rows = lv->colours.rows.p;
+        }
+        n1s[j] = sl.n1;
     }
     P.inv = h->coarse->inv.p;
     const SubLayout L = sub_layout(P.nlev, n1s);
@@ -1048,6 +1082,10 @@ int ocmg_level_create_csr(int problem, int64_t n, const int64_t *row_off,
         OCMG_LAUNCH(k_csr_ndiag, grid_for(n, kBlk), kBlk, 0, 0, n, lv->A.off.p,
                     lv->A.val.p, lv->W.p, lv->ndiag.p);
         OCMG_LAUNCH_CHECK();
+        // per call: the attribute is per device, and cheap to set
+        OCMG_CUDA(cudaFuncSetAttribute(k_csr_gs_sched_smem,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kCsrSmallSmemMax));
         {   // SELL-32 copy of A and W
             SellDev &S = lv->sell;
             S.nslices = (n + 31) / 32;

@@ -346,6 +346,61 @@ __global__ void k_gsell_gs_rows(int64_t nslots, int64_t slice0,
 // per group -- the coarse levels of a W-cycle are visited thousands of times)
 constexpr int64_t kCsrSmallN = 8192;
 
+// The same one-CTA sweep with the level staged in shared memory (rows,
+// columns, values, row_scaled, n_diag, x and r): the row updates of a group
+// are chains of dependent loads, and from global memory every link was an
+// L2 round trip (the W-cycle visits these bottom levels thousands of times
+// per cycle).  Identical arithmetic, so bit-identical to the global form.
+inline size_t csr_small_smem(int64_t n, int64_t nnz, int64_t ng) {
+    return (size_t)(nnz * (8 + 8 + 4) + n * (8 + 8 + 8 + 4) + (ng + 1) * 4 + (n + 1) * 4 + 64);
+}
+constexpr size_t kCsrSmallSmemMax = 200 * 1024;
+
+__global__ void __launch_bounds__(1024)
+    k_csr_gs_sched_smem(int ngroups, const int64_t *__restrict__ goff_g,
+                        const int32_t *__restrict__ rows_g, int reverse, int n,
+                        const int64_t *__restrict__ off_g, const int32_t *__restrict__ col_g,
+                        const double *__restrict__ val_g, const double *__restrict__ w_g,
+                        const double *__restrict__ nd_g, double *__restrict__ x_g,
+                        double *__restrict__ r_g) {
+    extern __shared__ __align__(16) double smc[];
+    const int nnz = (int)off_g[n];
+    double *val = smc, *w = val + nnz, *nd = w + nnz, *x = nd + n, *r = x + n;
+    int *col = reinterpret_cast<int *>(r + n), *off = col + nnz, *rows = off + n + 1,
+        *goff = rows + n;
+    for (int t = threadIdx.x; t < nnz; t += blockDim.x) {
+        val[t] = val_g[t];
+        w[t] = w_g[t];
+        col[t] = col_g[t];
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        nd[i] = nd_g[i];
+        x[i] = x_g[i];
+        r[i] = r_g[i];
+        rows[i] = rows_g[i];
+    }
+    for (int i = threadIdx.x; i <= n; i += blockDim.x) off[i] = (int)off_g[i];
+    for (int g = threadIdx.x; g <= ngroups; g += blockDim.x) goff[g] = (int)goff_g[g];
+    __syncthreads();
+    for (int g = 0; g < ngroups; ++g) {
+        const int l = reverse ? ngroups - 1 - g : g;
+        for (int k = goff[l] + threadIdx.x; k < goff[l + 1]; k += blockDim.x) {
+            const int i = rows[k];
+            const int b = off[i], e = off[i + 1];
+            double q = 0.0;
+            for (int t = b; t < e; ++t) q = __dadd_rn(q, __dmul_rn(w[t], r[col[t]]));
+            const double p = __ddiv_rn(q, nd[i]);
+            x[i] = __dadd_rn(x[i], p);
+            for (int t = b; t < e; ++t) r[col[t]] = __dsub_rn(r[col[t]], __dmul_rn(val[t], p));
+        }
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        x_g[i] = x[i];
+        r_g[i] = r[i];
+    }
+}
+
 __global__ void __launch_bounds__(1024)
     k_csr_gs_sched_small(int ngroups, const int64_t *__restrict__ goff,
                          const int32_t *__restrict__ rows, int reverse,

@@ -1,5 +1,6 @@
 // The coarse end of a multigrid cycle in ONE launch (structured Poisson,
-// multicolour NE-GS): a visit of level kt (<= 5) runs the whole recursion
+// multicolour NE-GS; below the structured levels possibly the generic CSR
+// level L2 over the coarsest L1): a visit of level kt (<= 5) runs the whole recursion
 // below it -- residual, pre-smoothing, restriction, the coarser visits
 // (twice for W), the coarse solve, prolongation, residual, post-smoothing --
 // in one CTA with every vector in shared memory.
@@ -25,6 +26,14 @@ struct SubLevel {
     int n1;
     const double *T;  // class tables (ocmg_p1.cuh layout)
     const double *C;  // multicolour table [49][2][29]
+    // generic (CSR) Poisson level below the structured ones (L2 when the
+    // coarsest level is the reference default L1): its operator, row_scaled,
+    // n_diag and multicolour groups, the arithmetic of k_csr_residual and
+    // k_csr_gs_sched_small
+    int csr, ngroups;
+    const int64_t *off, *goff;
+    const int32_t *col, *rows;
+    const double *val, *w, *nd;
 };
 
 // The block's work as a flat op list (built on the host by unrolling the
@@ -48,9 +57,15 @@ struct SubcycleParams {
 // shared-memory layout: per level j, X_j and B_j (2N doubles each); per
 // smoothed level j >= 1, the residual R_j as a zero-guarded (n1+2)^2 grid of
 // (state, adjoint) pairs
+// the generic level's CSR data staged in shared memory (from global memory
+// every access was an L2 round trip: the coarse inverse evicts L1)
+constexpr int kSubCsrNnz = 1024, kSubCsrRows = 64;
+constexpr int kSubCsrDoubles = 2 * kSubCsrNnz + kSubCsrRows + (2 * kSubCsrNnz + 3 * kSubCsrRows) / 2;
+
 struct SubLayout {
     int off_x[kSubMaxK], off_b[kSubMaxK], off_r[kSubMaxK];
     int off_a[kSubMaxK], off_c[kSubMaxK];  // A rows [49][28], mc table [49][2][29]
+    int off_csr;  // kSubCsrDoubles: val, w, n_diag, then ints col, grid col, off, goff, rows
     int total;  // doubles
 };
 
@@ -68,17 +83,36 @@ __host__ __device__ inline SubLayout sub_layout(int nlev, const int *n1s) {
         o += 2 * N;
         L.off_b[j] = o;
         o += 2 * N;
-        if (j >= 1) {  // the level's coefficients: shared memory, not L1 (the
-                       // coarse inverse streams through L1 every visit)
+        if (j >= 1 && n1 >= 7) {  // the level's coefficients: shared memory, not
+                                  // L1 (the coarse inverse streams through L1
+                                  // every visit); CSR levels (n1 < 7) read theirs
             L.off_a[j] = o;
             o += 49 * 28;
             L.off_c[j] = o;
             o += 49 * 2 * 29;
         }
     }
+    L.off_csr = o;
+    o += kSubCsrDoubles;
     L.total = o;
     return L;
 }
+
+// shared-memory view of the generic level's CSR data
+struct SubCsr {
+    double *val, *w, *nd;
+    int *col, *gcol, *off, *goff, *rows;
+    __device__ SubCsr(double *base) {
+        val = base;
+        w = val + kSubCsrNnz;
+        nd = w + kSubCsrNnz;
+        col = reinterpret_cast<int *>(nd + kSubCsrRows);
+        gcol = col + kSubCsrNnz;
+        off = gcol + kSubCsrNnz;
+        goff = off + kSubCsrRows;
+        rows = goff + kSubCsrRows;
+    }
+};
 
 namespace sub {
 
@@ -132,6 +166,49 @@ __device__ __forceinline__ void sweep(int n1, const double *Ct, double *X, doubl
             const int xi = iy * n1 + ix;
             X[xi] = __dadd_rn(X[xi], p[0]);
             X[N + xi] = __dadd_rn(X[N + xi], p[1]);
+        }
+        __syncthreads();
+    }
+}
+
+// generic level: r = -(A x) + b in CSR column order (k_csr_residual), into
+// the same guarded (state, adjoint) grid the structured ops use; gcol holds
+// each column's (grid pair, field) position in that grid
+__device__ __forceinline__ int grid_pos(int n1, int i) {
+    const int N = n1 * n1, f = i >= N, v = i - f * N, iy = v / n1, ix = v - iy * n1;
+    return 2 * ((iy + 1) * (n1 + 2) + ix + 1) + f;
+}
+__device__ __forceinline__ void residual_csr(const SubLevel &l, const SubCsr &c, const double *X,
+                                             const double *B, double2 *R) {
+    const int n = 2 * l.n1 * l.n1;
+    double *Rd = reinterpret_cast<double *>(R);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double s = 0.0;
+        for (int t = c.off[i]; t < c.off[i + 1]; ++t)
+            s = __dadd_rn(s, __dmul_rn(c.val[t], X[c.col[t]]));
+        Rd[grid_pos(l.n1, i)] = __dadd_rn(-s, B[i]);
+    }
+    __syncthreads();
+}
+// generic level, multicolour NE-GS: the colour groups in order (backward:
+// reversed), a group's rows in parallel, csr_gs_row's arithmetic
+__device__ __forceinline__ void sweep_csr(const SubLevel &l, const SubCsr &c, double *X,
+                                          double2 *R, bool forward) {
+    double *Rd = reinterpret_cast<double *>(R);
+    for (int g = 0; g < l.ngroups; ++g) {
+        const int gg = forward ? g : l.ngroups - 1 - g;
+        const int lo = c.goff[gg], hi = c.goff[gg + 1];
+        for (int k = lo + threadIdx.x; k < hi; k += blockDim.x) {
+            const int i = c.rows[k];
+            const int b = c.off[i], e = c.off[i + 1];
+            double q = 0.0;
+            for (int t = b; t < e; ++t) q = __dadd_rn(q, __dmul_rn(c.w[t], Rd[c.gcol[t]]));
+            const double p = __ddiv_rn(q, c.nd[i]);
+            X[i] = __dadd_rn(X[i], p);
+            for (int t = b; t < e; ++t) {
+                const int gj = c.gcol[t];
+                Rd[gj] = __dsub_rn(Rd[gj], __dmul_rn(c.val[t], p));
+            }
         }
         __syncthreads();
     }
@@ -224,7 +301,27 @@ __global__ void __launch_bounds__(kSubThreads, 1)
     const SubLayout L = sub_layout(P.nlev, n1s);
     for (int i = threadIdx.x; i < L.total; i += blockDim.x) sm[i] = 0.0;  // guards
     __syncthreads();
+    const SubCsr csr(sm + L.off_csr);
     for (int j = 1; j < P.nlev; ++j) {
+        if (P.lv[j].csr) {
+            const SubLevel &l = P.lv[j];
+            const int n = 2 * l.n1 * l.n1, nnz = (int)l.off[n];
+            for (int t = threadIdx.x; t < nnz; t += blockDim.x) {
+                csr.val[t] = l.val[t];
+                csr.w[t] = l.w[t];
+                csr.col[t] = l.col[t];
+                csr.gcol[t] = sub::grid_pos(l.n1, l.col[t]);
+            }
+            for (int i = threadIdx.x; i <= n; i += blockDim.x) {
+                csr.off[i] = (int)l.off[i];
+                if (i < n) {
+                    csr.nd[i] = l.nd[i];
+                    csr.rows[i] = l.rows[i];
+                }
+            }
+            for (int g = threadIdx.x; g <= l.ngroups; g += blockDim.x) csr.goff[g] = (int)l.goff[g];
+            continue;
+        }
         for (int i = threadIdx.x; i < 49 * 28; i += blockDim.x)
             sm[L.off_a[j] + i] = P.lv[j].T[kP1OffA + i];
         for (int i = threadIdx.x; i < 49 * 58; i += blockDim.x)
@@ -247,9 +344,19 @@ __global__ void __launch_bounds__(kSubThreads, 1)
         double *Xj = sm + L.off_x[j], *Bj = sm + L.off_b[j];
         double2 *Rj = reinterpret_cast<double2 *>(sm + L.off_r[j]);
         switch (op) {
-        case kOpResid: sub::residual(P.lv[j].n1, sm + L.off_a[j], Xj, Bj, Rj); break;
-        case kOpSweepF: sub::sweep(P.lv[j].n1, sm + L.off_c[j], Xj, Rj, true); break;
-        case kOpSweepB: sub::sweep(P.lv[j].n1, sm + L.off_c[j], Xj, Rj, false); break;
+        case kOpResid:
+            if (P.lv[j].csr)
+                sub::residual_csr(P.lv[j], csr, Xj, Bj, Rj);
+            else
+                sub::residual(P.lv[j].n1, sm + L.off_a[j], Xj, Bj, Rj);
+            break;
+        case kOpSweepF:
+        case kOpSweepB:
+            if (P.lv[j].csr)
+                sub::sweep_csr(P.lv[j], csr, Xj, Rj, op == kOpSweepF);
+            else
+                sub::sweep(P.lv[j].n1, sm + L.off_c[j], Xj, Rj, op == kOpSweepF);
+            break;
         case kOpRestrict: {  // B_{j-1} = R R_j, X_{j-1} = 0
             const int nc1 = P.lv[j - 1].n1;
             double *Xc = sm + L.off_x[j - 1];

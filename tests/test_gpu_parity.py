@@ -342,14 +342,17 @@ def test_strip_sweeps_match_single_gpu(k, ws):
     assert torch.equal(rg, r)
 
 
-@pytest.mark.parametrize("cycle,smoother,k", [("w", "lsgs", 8), ("v", "slsgs", 7),
-                                               ("w", "lsgs", 5)])
-def test_fused_coarse_block_is_bit_identical(cycle, smoother, k):
+@pytest.mark.parametrize("cycle,smoother,k,coarsest", [
+    ("w", "lsgs", 8, 3), ("v", "slsgs", 7, 3), ("w", "lsgs", 5, 3),
+    ("w", "lsgs", 8, 1), ("v", "lsgs", 6, 1), ("w", "slsgs", 5, 1),
+    ("v", "lsgs", 7, 2), ("w", "lsgs", 6, 2)])
+def test_fused_coarse_block_is_bit_identical(cycle, smoother, k, coarsest):
     """The one-launch coarse end of the cycle (ocmg_subcycle.cuh) reproduces
-    the per-level cycle bit for bit."""
+    the per-level cycle bit for bit, down to the reference's default
+    coarsest level L1 (the generic CSR level L2 inside the block)."""
     import ctypes
     cfg = P.CycleConfig(smoother=P.SmootherKind(smoother), cycle=cycle,
-                        coarsest_level=3, gs_mode="multicolour")
+                        coarsest_level=coarsest, gs_mode="multicolour")
     mg = P.build_solver("poisson", k, 1e-6, cfg)
     f = P.baseline_rhs(mg.finest, 0, add_sine=True)
     fn = _lib.load().ocmg__debug_hierarchy_fuse
