@@ -205,7 +205,9 @@ def run_reference_arm(args, ws, rank):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded U[-1,1])",
         "config": {"workload": f"poisson_control_L{args.level}_ne_gs_sweep",
-                   "sample": f"L{level} sweep", "alpha": args.alpha},
+                   "unknowns": osys.n, "alpha": args.alpha,
+                   "sample": f"full forward NE-GS sweep of L{level} per thread "
+                             "and step"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": nthreads,
                          "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -719,10 +721,14 @@ def main():
     ap.add_argument("--no-solve-l12-wavefront", action="store_true",
                     help="skip the exact-order (wavefront) W-cycle at L12")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-level", type=int, default=10)
-    ap.add_argument("--cpu-sweeps", type=int, default=10)
+    # the CPU arms sweep the headline level itself (same_config); --cpu-level
+    # only for quick local runs
+    ap.add_argument("--cpu-level", type=int, default=None)
+    ap.add_argument("--cpu-sweeps", type=int, default=5)
     ap.add_argument("--kernel-iters", type=int, default=5)
     args = ap.parse_args()
+    if args.cpu_level is None:
+        args.cpu_level = args.level
     if args.warmup < 3:
         print("warning: --warmup raised to 3 (timing rules)", file=sys.stderr)
         args.warmup = 3
