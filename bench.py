@@ -642,19 +642,23 @@ def run_gpu_arm(args, ws, rank, local):
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
+        # both NE-GS modes side by side: the exact (reference-order,
+        # wavefront) sweep is the reference arm's own order
+        other = "wavefront" if args.mode == "multicolour" else "multicolour"
+        result["modes"] = {args.mode: {"dof_per_s": value, "ms": t_step * 1e3,
+                                       "frac_hbm": achieved / hbm}}
+        st_o = P.make_smoother(dsys, "lsgs", gs_mode=other)
+        st_o.sweep(x, r)
+        t_o = time_events(lambda: st_o.sweep(x, r), 5, stream)
+        result["modes"][other] = {
+            "dof_per_s": n / t_o, "ms": t_o * 1e3,
+            "frac_hbm": BYTES["ne_gs"] * n / t_o / 1e9 / hbm}
         if not args.quick:
             from paper_1502_03917_b200.transfer import system_transfer
             coarse = P.build_poisson_system(args.level - 1, args.alpha)
             tr = system_transfer(coarse, dsys)
             result["kernels"] = kernel_table(dsys, coarse, tr, x, r, f,
                                              stream, args.kernel_iters, hbm)
-            other = "wavefront" if args.mode == "multicolour" else "multicolour"
-            result["modes"] = {args.mode: {"dof_per_s": value,
-                                           "ms": t_step * 1e3}}
-            st_o = P.make_smoother(dsys, "lsgs", gs_mode=other)
-            st_o.sweep(x, r)
-            t_o = time_events(lambda: st_o.sweep(x, r), 3, stream)
-            result["modes"][other] = {"dof_per_s": n / t_o, "ms": t_o * 1e3}
             # config 2: L10, NE-GS (both modes) vs NE-Jacobi, three alphas
             result["solve"] = []
             for a in (1.0, 1e-4, 1e-8):
@@ -677,13 +681,18 @@ def run_gpu_arm(args, ws, rank, local):
                 result["solve"] += sv
                 result["stokes_kernels"] = sk
             if not args.no_solve_l12:
-                # the exact-order W-cycle is north_star's target run (18
-                # cycles, the reference's count); ~9 s
+                # config 3 at the reference's default coarsest level L1
+                # (SURVEY §8(d)); the exact-order W-cycle is north_star's
+                # target run (18 cycles, the reference's count; its
+                # per-cycle iterates are pinned by tests/test_fullsize_gpu.py)
                 modes = ["multicolour"] + ([] if args.no_solve_l12_wavefront
                                            else ["wavefront"])
                 for m in modes:
                     result["solve"].append(solve_timing(
-                        args.level, args.alpha, "w", 3, m, True))
+                        args.level, args.alpha, "w", 1, m, True))
+                # and at coarsest L3 (round-1 runs used it)
+                result["solve"].append(solve_timing(
+                    args.level, args.alpha, "w", 3, "multicolour", True))
         if ws == 1 and not args.no_cpu:
             v, dt, ncpu = cpu_sweep_rate(args.cpu_level, args.cpu_sweeps,
                                          args.alpha)
@@ -708,10 +717,11 @@ def main():
     ap.add_argument("--alpha", type=float, default=1e-6)
     ap.add_argument("--mode", default="multicolour",
                     choices=["wavefront", "reference", "multicolour"])
-    ap.add_argument("--partition", default="replicas",
+    ap.add_argument("--partition", default=None,
                     choices=["replicas", "strips"],
-                    help="N>1: independent replicas (weak) or one L12 system "
-                         "in row strips with ghost exchange (strong)")
+                    help="N>1: one L12 system in row strips with ghost "
+                         "exchange (strong scaling, the default) or N "
+                         "independent replicas (weak)")
     ap.add_argument("--quick", action="store_true",
                     help="headline only (no kernel table / solves)")
     ap.add_argument("--no-stokes-l10", action="store_true",
@@ -729,6 +739,8 @@ def main():
     args = ap.parse_args()
     if args.cpu_level is None:
         args.cpu_level = args.level
+    if args.partition is None:
+        args.partition = "strips" if args.gpus > 1 else "replicas"
     if args.warmup < 3:
         print("warning: --warmup raised to 3 (timing rules)", file=sys.stderr)
         args.warmup = 3

@@ -239,8 +239,9 @@ class LoopbackComm:
 
 class DistComm:
     """One rank per process, torch.distributed (NCCL over NVLink for CUDA
-    tensors): ghost rows by isend/irecv straight into the full-size vectors,
-    all-gather by one broadcast per rank and field, sums by all_reduce."""
+    tensors): ghost rows by grouped isend/irecv straight into the full-size
+    vectors, the gather by one padded all_gather_into_tensor, sums by
+    all_reduce."""
 
     def __init__(self, group=None, device="cuda"):
         self.group, self.device = group, device
@@ -266,14 +267,28 @@ class DistComm:
                 r.wait()
 
     def allgather(self, states, level, name):
+        """One all_gather_into_tensor of every rank's rows (both fields),
+        each padded to the longest strip, then scattered into place."""
+        import torch
         import torch.distributed as dist
         (st,) = states
         v = getattr(st, name)[level]
         n1 = st.n1[level]
-        for p in range(st.world_size):
-            a, b = st.all_bounds[level][p]
-            for f_view in _rows(v, n1, a, b):
-                dist.broadcast(f_view, p, group=self.group)
+        bnds = st.all_bounds[level]
+        mrows = max(b - a for a, b in bnds)
+        a, b = bnds[st.rank]
+        send = torch.zeros(2, mrows, n1, dtype=v.dtype, device=v.device)
+        for f, rows in enumerate(_rows(v, n1, a, b)):
+            send[f, :b - a] = rows.view(b - a, n1)
+        recv = torch.empty(st.world_size * 2 * mrows * n1, dtype=v.dtype,
+                           device=v.device)
+        dist.all_gather_into_tensor(recv, send.reshape(-1), group=self.group)
+        recv = recv.view(st.world_size, 2, mrows, n1)
+        for p, (a, b) in enumerate(bnds):
+            if p == st.rank:
+                continue
+            for f, rows in enumerate(_rows(v, n1, a, b)):
+                rows.copy_(recv[p, f, :b - a].reshape(-1))
 
     def allreduce(self, values):
         import torch
