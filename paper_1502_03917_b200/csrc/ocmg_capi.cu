@@ -364,6 +364,13 @@ void run_schedule(const ocmg_level *lv, const Schedule &S, bool reverse,
         // small level: every group in one CTA, __syncthreads between groups;
         // staged in shared memory when it fits
         const size_t sm = csr_small_smem(lv->n, lv->A.nnz, nb);
+        if (warp_rows && lv->n <= kCsrWarpN && sm <= kCsrSmallSmemMax) {
+            OCMG_LAUNCH(k_csr_gs_warp_small, 1, 32, sm, s, (int)nb, S.doff.p, S.rows.p,
+                        reverse ? 1 : 0, (int)lv->n, lv->A.off.p, lv->A.col.p, lv->A.val.p,
+                        lv->W.p, lv->ndiag.p, x, r);
+            OCMG_LAUNCH_CHECK();
+            return;
+        }
         if (sm <= kCsrSmallSmemMax) {
             const int nt = lv->n < 1024 ? (int)(32 * ((lv->n + 31) / 32)) : 1024;
             OCMG_LAUNCH(k_csr_gs_sched_smem, 1, nt, sm, s, (int)nb, S.doff.p, S.rows.p,
@@ -1084,6 +1091,9 @@ int ocmg_level_create_csr(int problem, int64_t n, const int64_t *row_off,
         OCMG_LAUNCH_CHECK();
         // per call: the attribute is per device, and cheap to set
         OCMG_CUDA(cudaFuncSetAttribute(k_csr_gs_sched_smem,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kCsrSmallSmemMax));
+        OCMG_CUDA(cudaFuncSetAttribute(k_csr_gs_warp_small,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)kCsrSmallSmemMax));
         {   // SELL-32 copy of A and W

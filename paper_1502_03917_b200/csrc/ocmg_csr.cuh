@@ -356,6 +356,76 @@ inline size_t csr_small_smem(int64_t n, int64_t nnz, int64_t ng) {
 }
 constexpr size_t kCsrSmallSmemMax = 200 * 1024;
 
+// Exact order (wavefront mode) on a tiny generic level (Poisson L2: 50
+// unknowns whose dependency DAG is nearly a chain): ONE warp, the level in
+// shared memory, the rows of the schedule one after another with
+// k_csr_gs_rows_warp's arithmetic (lanes over a row's entries, butterfly sum,
+// FMA; the 1e-12 mode).  A CTA barrier per dependency level cost more than
+// the row.
+constexpr int64_t kCsrWarpN = 256;
+__global__ void __launch_bounds__(32)
+    k_csr_gs_warp_small(int ngroups, const int64_t *__restrict__ goff_g,
+                        const int32_t *__restrict__ rows_g, int reverse, int n,
+                        const int64_t *__restrict__ off_g, const int32_t *__restrict__ col_g,
+                        const double *__restrict__ val_g, const double *__restrict__ w_g,
+                        const double *__restrict__ nd_g, double *__restrict__ x_g,
+                        double *__restrict__ r_g) {
+    extern __shared__ __align__(16) double smc[];
+    const int lane = threadIdx.x;
+    const int nnz = (int)off_g[n];
+    double *val = smc, *w = val + nnz, *nd = w + nnz, *x = nd + n, *r = x + n;
+    int *col = reinterpret_cast<int *>(r + n), *off = col + nnz, *rows = off + n + 1,
+        *goff = rows + n;
+    // staging: every load of a pass in flight at once (a dependent load per
+    // group of the schedule cost ~20 us at L2)
+#pragma unroll 4
+    for (int t = lane; t < nnz; t += 32) {
+        val[t] = val_g[t];
+        w[t] = w_g[t];
+        col[t] = col_g[t];
+    }
+#pragma unroll 4
+    for (int i = lane; i < n; i += 32) {
+        nd[i] = nd_g[i];
+        x[i] = x_g[i];
+        r[i] = r_g[i];
+        rows[i] = rows_g[i];
+    }
+    for (int i = lane; i <= n; i += 32) off[i] = (int)off_g[i];
+    for (int g = lane; g <= ngroups; g += 32) goff[g] = (int)goff_g[g];
+    __syncwarp();
+    // rows in schedule order: groups forward (or reversed for a reverse sweep)
+    const int m = goff[ngroups];
+    for (int k0 = 0; k0 < m; ++k0) {
+        int k = k0;
+        if (reverse) {  // k0-th row of the reversed group order
+            int g = 0, acc = 0;
+            for (g = ngroups - 1; g >= 0; --g) {
+                const int len = goff[g + 1] - goff[g];
+                if (k0 < acc + len) break;
+                acc += len;
+            }
+            k = goff[g] + (k0 - acc);
+        }
+        const int i = rows[k], b = off[i], e = off[i + 1];
+        double q = 0.0;
+        for (int t = b + lane; t < e; t += 32) q = fma(w[t], r[col[t]], q);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+        const double p = q / nd[i];
+        if (lane == 0) x[i] += p;
+        for (int t = b + lane; t < e; t += 32) {
+            const int j = col[t];
+            r[j] = fma(-val[t], p, r[j]);
+        }
+        __syncwarp();
+    }
+    for (int i = lane; i < n; i += 32) {
+        x_g[i] = x[i];
+        r_g[i] = r[i];
+    }
+}
+
 __global__ void __launch_bounds__(1024)
     k_csr_gs_sched_smem(int ngroups, const int64_t *__restrict__ goff_g,
                         const int32_t *__restrict__ rows_g, int reverse, int n,
@@ -368,11 +438,13 @@ __global__ void __launch_bounds__(1024)
     double *val = smc, *w = val + nnz, *nd = w + nnz, *x = nd + n, *r = x + n;
     int *col = reinterpret_cast<int *>(r + n), *off = col + nnz, *rows = off + n + 1,
         *goff = rows + n;
+#pragma unroll 4
     for (int t = threadIdx.x; t < nnz; t += blockDim.x) {
         val[t] = val_g[t];
         w[t] = w_g[t];
         col[t] = col_g[t];
     }
+#pragma unroll 4
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         nd[i] = nd_g[i];
         x[i] = x_g[i];
@@ -391,7 +463,23 @@ __global__ void __launch_bounds__(1024)
             for (int t = b; t < e; ++t) q = __dadd_rn(q, __dmul_rn(w[t], r[col[t]]));
             const double p = __ddiv_rn(q, nd[i]);
             x[i] = __dadd_rn(x[i], p);
-            for (int t = b; t < e; ++t) r[col[t]] = __dsub_rn(r[col[t]], __dmul_rn(val[t], p));
+            // a row's columns are distinct: batches of loads before their
+            // stores (one read-modify-write at a time serialised on the
+            // shared-memory latency, 1.5 us per dependency level at L2)
+            constexpr int kB = 8;
+            for (int t0 = b; t0 < e; t0 += kB) {
+                double rv[kB];
+                int jv[kB];
+#pragma unroll
+                for (int u = 0; u < kB; ++u)
+                    if (t0 + u < e) {
+                        jv[u] = col[t0 + u];
+                        rv[u] = r[jv[u]];
+                    }
+#pragma unroll
+                for (int u = 0; u < kB; ++u)
+                    if (t0 + u < e) r[jv[u]] = __dsub_rn(rv[u], __dmul_rn(val[t0 + u], p));
+            }
         }
         __syncthreads();
     }

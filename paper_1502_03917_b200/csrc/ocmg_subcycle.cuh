@@ -205,9 +205,19 @@ __device__ __forceinline__ void sweep_csr(const SubLevel &l, const SubCsr &c, do
             for (int t = b; t < e; ++t) q = __dadd_rn(q, __dmul_rn(c.w[t], Rd[c.gcol[t]]));
             const double p = __ddiv_rn(q, c.nd[i]);
             X[i] = __dadd_rn(X[i], p);
-            for (int t = b; t < e; ++t) {
-                const int gj = c.gcol[t];
-                Rd[gj] = __dsub_rn(Rd[gj], __dmul_rn(c.val[t], p));
+            constexpr int kB = 8;  // distinct columns: loads batched before stores
+            for (int t0 = b; t0 < e; t0 += kB) {
+                double rv[kB];
+                int gv[kB];
+#pragma unroll
+                for (int u = 0; u < kB; ++u)
+                    if (t0 + u < e) {
+                        gv[u] = c.gcol[t0 + u];
+                        rv[u] = Rd[gv[u]];
+                    }
+#pragma unroll
+                for (int u = 0; u < kB; ++u)
+                    if (t0 + u < e) Rd[gv[u]] = __dsub_rn(rv[u], __dmul_rn(c.val[t0 + u], p));
             }
         }
         __syncthreads();
