@@ -73,7 +73,17 @@ constexpr int LAG = (NC - 1) * C + 1 + K;
 constexpr int D = MCS_D;           // cp.async prefetch distance (supersteps)
 // live rows: the K leaving (LAG behind) .. the K D + K rows in flight
 constexpr int RING = K * D + K + LAG + 1;
-constexpr int NT = 32 * (NC + 1);  // 7 colour warps + the boundary-column warp
+#ifndef MCS_WPC
+#define MCS_WPC 1
+#endif
+// warps per colour: each takes K / WPC of the colour's K rows per superstep.
+// WPC = 2 (15 warps of 128 registers instead of 8 of 240) measured the same
+// 0.439 ms at L12 as WPC = 1: the superstep is bound by the shared-memory
+// pipe (~1100 wavefronts of ~2150 cycles) and issue, not by latency hiding
+constexpr int WPC = MCS_WPC;
+constexpr int KW = K / WPC;          // rows per colour warp and superstep
+static_assert(K % WPC == 0, "rows per superstep split evenly over a colour's warps");
+constexpr int NT = 32 * (NC * WPC + 1);  // colour warps + the boundary-column warp
 constexpr int W = MCS_W;           // owned columns per CTA (at most)
 constexpr int STRIDE = W + 2 * H + 2;  // r ring row: columns xl-1 .. xr
 constexpr int RS = STRIDE * 16;    // r ring row bytes: (state, adjoint) pairs
@@ -296,8 +306,9 @@ __global__ void __launch_bounds__(mcs::NT, 1) k_p1_mc_sweep(const __grid_constan
     // 7 (the boundary warp): its lane (side, q', i) takes the one vertex of
     // colour-warp q' row i in the three columns at that side, with the
     // class row from shared memory.
-    const bool bw = q == NC;
-    const int qq = bw ? (lane % 14) / 2 : q;           // the colour warp emulated
+    const bool bw = q == NC * WPC;
+    const int qq = bw ? (lane % 14) / 2 : q / WPC;     // the colour (warp) emulated
+    const int i0 = bw ? 0 : (q % WPC) * KW;            // colour warp: its first row
     const int bi = bw ? lane & 1 : 0;                  // boundary warp: its row i
     const int side = bw ? (lane < 14 ? 0 : lane < 28 ? 1 : 2) : 0;  // left, right, none
     const bool bside = bw && ((side == 0 && xl == 0) || (side == 1 && xr == n1));
@@ -374,54 +385,56 @@ __global__ void __launch_bounds__(mcs::NT, 1) k_p1_mc_sweep(const __grid_constan
         auto int_row = [&](int i) { return (unsigned)(y + i - 3) <= (unsigned)(n1 - 7); };
         auto int_col = [&](int x) { return (unsigned)(x - 3) <= (unsigned)(n1 - 7); };
         if (!bw) {
-            int xi[K];
-            bool act[K];
+            int xi[KW];
+            bool act[KW];
             bool allint = true;
 #pragma unroll
-            for (int i = 0; i < K; ++i) {
+            for (int ii = 0; ii < KW; ++ii) {
+                const int i = i0 + ii;
                 const int oi = (o - 2 * i + 7 * K) % 7;
-                xi[i] = xbase + oi;
-                act[i] = in_rows(i) && (unsigned)(xi[i] - cxl) < (unsigned)(cxr - cxl);
+                xi[ii] = xbase + oi;
+                act[ii] = in_rows(i) && (unsigned)(xi[ii] - cxl) < (unsigned)(cxr - cxl);
                 allint = allint && int_row(i);
                 // boundary columns of interior rows: the boundary warp's
-                act[i] = act[i] && (!int_row(i) || int_col(xi[i]));
+                act[ii] = act[ii] && (!int_row(i) || int_col(xi[ii]));
             }
             if (allint) {  // warp-uniform: every computed lane has the interior class
-                double2 v[K][7];
+                double2 v[KW][7];
 #pragma unroll
-                for (int i = 0; i < K; ++i) load_v(i, xi[i], v[i]);
-                double pa[K], pb[K];  // first / second unknown in sweep order
+                for (int ii = 0; ii < KW; ++ii) load_v(i0 + ii, xi[ii], v[ii]);
+                double pa[KW], pb[KW];  // first / second unknown in sweep order
 #pragma unroll
-                for (int i = 0; i < K; ++i) pa[i] = node_update_u<FWD ? 0 : 1>(v[i], cu);
+                for (int ii = 0; ii < KW; ++ii) pa[ii] = node_update_u<FWD ? 0 : 1>(v[ii], cu);
 #pragma unroll
-                for (int i = 0; i < K; ++i) pb[i] = node_update_u<FWD ? 1 : 0>(v[i], cu);
+                for (int ii = 0; ii < KW; ++ii) pb[ii] = node_update_u<FWD ? 1 : 0>(v[ii], cu);
 #pragma unroll
-                for (int i = 0; i < K; ++i)
-                    if (act[i]) {
-                        store_v(i, xi[i], v[i]);
-                        if (owned(i, xi[i])) x_update(i, xi[i], pa[i], pb[i]);
+                for (int ii = 0; ii < KW; ++ii)
+                    if (act[ii]) {
+                        store_v(i0 + ii, xi[ii], v[ii]);
+                        if (owned(i0 + ii, xi[ii])) x_update(i0 + ii, xi[ii], pa[ii], pb[ii]);
                     }
             } else {  // a boundary row: per-lane class rows from the global table
 #pragma unroll
-                for (int i = 0; i < K; ++i) {
+                for (int ii = 0; ii < KW; ++ii) {
+                    const int i = i0 + ii;
                     if (!in_rows(i)) continue;  // warp-uniform
                     double2 v[7];
-                    load_v(i, xi[i], v);
+                    load_v(i, xi[ii], v);
                     double pa, pb;
                     if (int_row(i)) {
                         pa = node_update_u<FWD ? 0 : 1>(v, cu);
                         pb = node_update_u<FWD ? 1 : 0>(v, cu);
                     } else {
-                        const int xc = min(max(xi[i], 0), n1 - 1);
+                        const int xc = min(max(xi[ii], 0), n1 - 1);
                         const int yc = min(max(y + i, 0), n1 - 1);
                         const double *Cc =
                             P.C + (7 * p1_axis_class(yc, n1) + p1_axis_class(xc, n1)) * 58;
                         pa = node_update(v, Cc + (FWD ? 0 : 29));
                         pb = node_update(v, Cc + (FWD ? 29 : 0));
                     }
-                    if (act[i]) {
-                        store_v(i, xi[i], v);
-                        if (owned(i, xi[i])) x_update(i, xi[i], pa, pb);
+                    if (act[ii]) {
+                        store_v(i, xi[ii], v);
+                        if (owned(i, xi[ii])) x_update(i, xi[ii], pa, pb);
                     }
                 }
             }
