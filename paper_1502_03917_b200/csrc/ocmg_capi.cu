@@ -72,6 +72,10 @@ struct ocmg_level {
     Schedule sched[2];  // 0 forward, 1 backward
     Schedule colours;
     bool has_colours = false;
+    // tiny levels (n <= kDenseN): dense sweep maps [mode: 0 exact, 1
+    // multicolour][0 forward, 1 backward], each S^T then T^T (n*n each)
+    DevBuf<double> dense[2][2];
+    bool has_dense = false;
     // Vanka patches (ocmg_level_set_vanka)
     int64_t vk_np = 0;
     int vk_mmax = 0;
@@ -556,6 +560,16 @@ void level_ne_gs(const ocmg_level *lv, int mode, bool forward, double *x,
         OCMG_LAUNCH_CHECK();
         return;
     }
+    if (mode != OCMG_GS_REFERENCE && lv->has_dense &&
+        (mode == OCMG_GS_WAVEFRONT || lv->has_colours)) {
+        // tiny level: the sweep as its dense map (k_dense_sweep)
+        const DevBuf<double> &D = lv->dense[mode == OCMG_GS_MULTICOLOUR][forward ? 0 : 1];
+        const int n = (int)lv->n;
+        OCMG_LAUNCH(k_dense_sweep, 1, n < 256 ? (int)(32 * ((n + 31) / 32)) : 256, 0, s, n,
+                    D.p, D.p + (int64_t)n * n, x, r);
+        OCMG_LAUNCH_CHECK();
+        return;
+    }
     if (mode == OCMG_GS_MULTICOLOUR) {
         OCMG_REQUIRE(lv->has_colours,
                      "multicolour NE-GS needs a level created with colouring");
@@ -997,6 +1011,10 @@ void setup_subcycle(ocmg_hierarchy *h) {
             sl.nd = lv->ndiag.p;
             sl.goff = lv->colours.doff.p;
             sl.rows = lv->colours.rows.p;
+            if (lv->has_dense) {  // the same dense maps as level_ne_gs
+                sl.dense[0] = lv->dense[1][0].p;
+                sl.dense[1] = lv->dense[1][1].p;
+            }
         }
         n1s[j] = sl.n1;
     }
@@ -1128,6 +1146,35 @@ int ocmg_level_create_csr(int problem, int64_t n, const int64_t *row_off,
             build_group_sell(lv->sched[0], n, row_off, lv->A, lv->W.p);
             build_group_sell(lv->sched[1], n, row_off, lv->A, lv->W.p);
             if (want_colouring) build_group_sell(lv->colours, n, row_off, lv->A, lv->W.p);
+        }
+        if (n <= kDenseN) {
+            // dense sweep maps (k_dense_sweep): columns from the sequential
+            // sweep of each unit residual, exact order and colour order
+            const size_t sm = csr_small_smem(n, lv->A.nnz, n + 1);
+            if (sm <= kCsrSmallSmemMax) {
+                OCMG_CUDA(cudaFuncSetAttribute(k_csr_gs_sched_smem,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)kCsrSmallSmemMax));
+                const int nt = (int)(32 * ((n + 31) / 32));
+                for (int md = 0; md < 2; ++md) {
+                    if (md == 1 && !want_colouring) continue;
+                    for (int dir = 0; dir < 2; ++dir) {
+                        const Schedule &S = md == 0 ? lv->sched[dir] : lv->colours;
+                        const int reverse = md == 1 && dir == 1;
+                        DevBuf<double> &D = lv->dense[md][dir];
+                        D.alloc(2 * n * n);
+                        OCMG_LAUNCH(k_dense_unit, grid_for(n * n, kBlk), kBlk, 0, 0, (int)n,
+                                    D.p, D.p + n * n);
+                        OCMG_LAUNCH(k_csr_gs_sched_smem, (unsigned)n, nt, sm, 0,
+                                    (int)S.off.size() - 1, S.doff.p, S.rows.p, reverse,
+                                    (int)n, lv->A.off.p, lv->A.col.p, lv->A.val.p, lv->W.p,
+                                    lv->ndiag.p, D.p, D.p + n * n, n);
+                        OCMG_LAUNCH_CHECK();
+                    }
+                }
+                OCMG_CUDA(cudaDeviceSynchronize());
+                lv->has_dense = true;
+            }
         }
         lv->partial.alloc(kRedGrid);
         lv->scal.alloc(8);

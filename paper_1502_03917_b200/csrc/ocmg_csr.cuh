@@ -363,6 +363,43 @@ constexpr size_t kCsrSmallSmemMax = 200 * 1024;
 // FMA; the 1e-12 mode).  A CTA barrier per dependency level cost more than
 // the row.
 constexpr int64_t kCsrWarpN = 256;
+
+// Tiny generic levels as dense maps.  A sweep in a fixed order is linear in
+// the entering (x, r): x += S r, r <- T r.  For levels of at most kDenseN
+// unknowns (Poisson L2: 50, Stokes L2: 246) S and T are built once at level
+// creation by running the sequential sweep (k_csr_gs_sched_smem, the
+// reference's arithmetic) on the n unit residuals in one batched launch, and
+// a sweep becomes two dense products (rounding differs from the sequential
+// sweep by ~1e-16 per entry: the exact mode's 1e-12 bar, and the multicolour
+// mode's own smoother).  The L2 sweeps were ~110 ms of an exact L12 W-cycle
+// at coarsest L1 (4096 sweeps of a 50-row DAG that is nearly a chain).
+// Stored transposed: ST[j * n + i] = S[i][j], so thread i reads coalesced.
+constexpr int64_t kDenseN = 256;
+__global__ void __launch_bounds__(256)
+    k_dense_sweep(int n, const double *__restrict__ ST, const double *__restrict__ TT,
+                  double *__restrict__ x, double *__restrict__ r) {
+    __shared__ double rs[kDenseN];
+    for (int j = threadIdx.x; j < n; j += blockDim.x) rs[j] = r[j];
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double ds = 0.0, rt = 0.0;
+        for (int j = 0; j < n; ++j) {
+            const double rj = rs[j];
+            ds = fma(__ldg(ST + (int64_t)j * n + i), rj, ds);
+            rt = fma(__ldg(TT + (int64_t)j * n + i), rj, rt);
+        }
+        x[i] += ds;
+        r[i] = rt;
+    }
+}
+// unit residuals for the batched build: R[b * n + i] = (i == b), X = 0
+__global__ void k_dense_unit(int n, double *X, double *R) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < (int64_t)n * n) {
+        X[t] = 0.0;
+        R[t] = (t / n == t % n) ? 1.0 : 0.0;
+    }
+}
 __global__ void __launch_bounds__(32)
     k_csr_gs_warp_small(int ngroups, const int64_t *__restrict__ goff_g,
                         const int32_t *__restrict__ rows_g, int reverse, int n,
@@ -432,10 +469,12 @@ __global__ void __launch_bounds__(1024)
                         const int64_t *__restrict__ off_g, const int32_t *__restrict__ col_g,
                         const double *__restrict__ val_g, const double *__restrict__ w_g,
                         const double *__restrict__ nd_g, double *__restrict__ x_g,
-                        double *__restrict__ r_g) {
+                        double *__restrict__ r_g, int64_t batch = 0) {
     extern __shared__ __align__(16) double smc[];
     const int nnz = (int)off_g[n];
     double *val = smc, *w = val + nnz, *nd = w + nnz, *x = nd + n, *r = x + n;
+    x_g += blockIdx.x * batch;  // batched: one independent (x, r) per block
+    r_g += blockIdx.x * batch;
     int *col = reinterpret_cast<int *>(r + n), *off = col + nnz, *rows = off + n + 1,
         *goff = rows + n;
 #pragma unroll 4

@@ -34,6 +34,8 @@ struct SubLevel {
     const int64_t *off, *goff;
     const int32_t *col, *rows;
     const double *val, *w, *nd;
+    const double *dense[2];  // multicolour sweep as dense maps S^T, T^T
+                             // (forward, backward; k_dense_sweep), or null
 };
 
 // The block's work as a flat op list (built on the host by unrolling the
@@ -60,7 +62,8 @@ struct SubcycleParams {
 // the generic level's CSR data staged in shared memory (from global memory
 // every access was an L2 round trip: the coarse inverse evicts L1)
 constexpr int kSubCsrNnz = 1024, kSubCsrRows = 64;
-constexpr int kSubCsrDoubles = 2 * kSubCsrNnz + kSubCsrRows + (2 * kSubCsrNnz + 3 * kSubCsrRows) / 2;
+constexpr int kSubCsrDoubles =
+    2 * kSubCsrNnz + 2 * kSubCsrRows + (2 * kSubCsrNnz + 3 * kSubCsrRows) / 2;
 
 struct SubLayout {
     int off_x[kSubMaxK], off_b[kSubMaxK], off_r[kSubMaxK];
@@ -100,13 +103,14 @@ __host__ __device__ inline SubLayout sub_layout(int nlev, const int *n1s) {
 
 // shared-memory view of the generic level's CSR data
 struct SubCsr {
-    double *val, *w, *nd;
+    double *val, *w, *nd, *rt;
     int *col, *gcol, *off, *goff, *rows;
     __device__ SubCsr(double *base) {
         val = base;
         w = val + kSubCsrNnz;
         nd = w + kSubCsrNnz;
-        col = reinterpret_cast<int *>(nd + kSubCsrRows);
+        rt = nd + kSubCsrRows;  // the entering residual of a dense-map sweep
+        col = reinterpret_cast<int *>(rt + kSubCsrRows);
         gcol = col + kSubCsrNnz;
         off = gcol + kSubCsrNnz;
         goff = off + kSubCsrRows;
@@ -190,8 +194,30 @@ __device__ __forceinline__ void residual_csr(const SubLevel &l, const SubCsr &c,
     }
     __syncthreads();
 }
+// generic level, multicolour NE-GS as its dense map (k_dense_sweep's
+// arithmetic: x += S r, r <- T r, sums over j in order)
+__device__ __forceinline__ void sweep_dense(const SubLevel &l, const SubCsr &c, double *X,
+                                            double2 *R, bool forward) {
+    double *Rd = reinterpret_cast<double *>(R);
+    const int n = 2 * l.n1 * l.n1;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) c.rt[j] = Rd[grid_pos(l.n1, j)];
+    __syncthreads();
+    const double *ST = l.dense[forward ? 0 : 1], *TT = ST + (int64_t)n * n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double ds = 0.0, rt = 0.0;
+        for (int j = 0; j < n; ++j) {
+            const double rj = c.rt[j];
+            ds = fma(__ldg(ST + (int64_t)j * n + i), rj, ds);
+            rt = fma(__ldg(TT + (int64_t)j * n + i), rj, rt);
+        }
+        X[i] += ds;
+        Rd[grid_pos(l.n1, i)] = rt;
+    }
+    __syncthreads();
+}
 // generic level, multicolour NE-GS: the colour groups in order (backward:
-// reversed), a group's rows in parallel, csr_gs_row's arithmetic
+// reversed), a group's rows in parallel, csr_gs_row's arithmetic (used when
+// the level has no dense maps)
 __device__ __forceinline__ void sweep_csr(const SubLevel &l, const SubCsr &c, double *X,
                                           double2 *R, bool forward) {
     double *Rd = reinterpret_cast<double *>(R);
@@ -362,7 +388,9 @@ __global__ void __launch_bounds__(kSubThreads, 1)
             break;
         case kOpSweepF:
         case kOpSweepB:
-            if (P.lv[j].csr)
+            if (P.lv[j].csr && P.lv[j].dense[0])
+                sub::sweep_dense(P.lv[j], csr, Xj, Rj, op == kOpSweepF);
+            else if (P.lv[j].csr)
                 sub::sweep_csr(P.lv[j], csr, Xj, Rj, op == kOpSweepF);
             else
                 sub::sweep(P.lv[j].n1, sm + L.off_c[j], Xj, Rj, op == kOpSweepF);

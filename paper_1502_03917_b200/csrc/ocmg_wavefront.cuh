@@ -142,6 +142,9 @@ __device__ __forceinline__ void st_release(int *p, int v) {
 
 // per-CTA constants, shared by the stage functions
 struct WfBand {
+    double *hsink;  // this band's dummy hand-off slots: non-publishing lanes
+                    // store there unconditionally (a guarded store cost the
+                    // chain 30-40 cycles per step)
     int n1, b, iy0, nreal;
     int64_t N;
     const double *sA, *sW, *sN;  // shared tables
@@ -180,16 +183,15 @@ __device__ __forceinline__ double wf_sel(bool c, double a, double b) {
     return __longlong_as_double((__double_as_longlong(a) & m) | (__double_as_longlong(b) & ~m));
 }
 
-// stores under a predicate without a branch region (a guarded store in C++
-// becomes BSSY/BRA/BSYNC, which serialises the stage's steps)
+// guarded stores (kept as plain C++: inline asm with a memory clobber stopped
+// the compiler from moving the next loads above them, 15-30 cycles per step)
 __device__ __forceinline__ void wf_sts(double *p, double v, bool pred) {
-    const unsigned a = (unsigned)__cvta_generic_to_shared(p);
-    asm volatile("{.reg .pred q; setp.ne.b32 q, %2, 0; @q st.shared.f64 [%0], %1;}"
-                 ::"r"(a), "d"(v), "r"((int)pred) : "memory");
+    // a plain guarded store: the compiler predicates it, and (unlike inline
+    // asm with a memory clobber) may still move the next loads above it
+    if (pred) *p = v;
 }
 __device__ __forceinline__ void wf_stg(double *p, double v, bool pred) {
-    asm volatile("{.reg .pred q; setp.ne.b32 q, %2, 0; @q st.global.f64 [%0], %1;}"
-                 ::"l"(p), "d"(v), "r"((int)pred) : "memory");
+    if (pred) *p = v;
 }
 
 // window accessors (processing-frame band row i, slot s)
@@ -289,9 +291,9 @@ __device__ __forceinline__ void wf_chain(const WfBand &B, WfChain &S, const doub
     for (int s = 0; s < CW; ++s) wf_sts(pw + (ip + 2) * SS + ((tau0 + s) & (WS - 1)), pout[s], i < nrows);
     if (ho) {
         const bool pub = i == REAL - 2 || i == REAL - 1;
-        double *h = ho + (int64_t)(tau0 + SO) * HO + hoff + (pub ? i - (REAL - 2) : 0);
+        double *h = pub ? ho + (int64_t)(tau0 + SO) * HO + hoff + (i - (REAL - 2)) : B.hsink;
 #pragma unroll
-        for (int s = 0; s < CW; ++s) wf_stg(h + s * HO, pout[s], pub);
+        for (int s = 0; s < CW; ++s) h[s * HO] = pout[s];
     }
 }
 
@@ -308,7 +310,7 @@ template <bool BWD, bool FAST>
 __device__ __forceinline__ void wf_gstage(const WfBand &B, int F, int tau0, int nrows,
                                           double *gw, double *ho) {
     using namespace wf;
-    constexpr int H = CW / 2;
+    constexpr int H = CW;  // one pass of 8 outputs (67 vs 73 cycles/step for two of 4)
     const int i = threadIdx.x & 31;
     const int ii = min(i, nrows - 1);  // address row (idle lanes read a valid row)
     // this lane's row class with an interior column class (FAST: every
@@ -321,7 +323,7 @@ __device__ __forceinline__ void wf_gstage(const WfBand &B, int F, int tau0, int 
 #pragma unroll
         for (int e = 0; e < 7; ++e) w[f][e] = Wi[f * 7 + (BWD ? 6 - e : e)];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < CW / H; ++h) {
         const int t0 = tau0 + h * H;
         // row i-1: slots t0-3 .. t0+H-3; row i: t0-1 .. t0+H; row i+1: t0+2 .. t0+H+2
         double up[2][H + 1], md[2][H + 2], dn[2][H + 1];
@@ -359,11 +361,11 @@ __device__ __forceinline__ void wf_gstage(const WfBand &B, int F, int tau0, int 
 #pragma unroll
         for (int s = 0; s < H; ++s) wf_sts(gw + ii * SS + ((t0 + s) & (WS - 1)), out[s], i < nrows);
         if (ho) {  // G1 only: r_entry of row 28 for band b+1
-            double *h = ho + (int64_t)(t0 + SO) * HO + 6;
+            double *h = i == REAL - 1 ? ho + (int64_t)(t0 + SO) * HO + 6 : B.hsink;
 #pragma unroll
             for (int s = 0; s < H; ++s) {
-                wf_stg(h + s * HO, md[0][s + 1], i == REAL - 1);
-                wf_stg(h + s * HO + 1, md[1][s + 1], i == REAL - 1);
+                h[s * HO] = md[0][s + 1];
+                h[s * HO + 1] = md[1][s + 1];
             }
         }
     }
@@ -440,9 +442,9 @@ __device__ __forceinline__ void wf_astage(const WfBand &B, int FP, int tau0, int
             wf_sts(&wf_re(B, 0, i, tau), out[0][s], ok);
             wf_sts(&wf_re(B, 1, i, tau), out[1][s], ok);
             if (ho) {
-                double *h = ho + (int64_t)(tau + SO) * HO + hoff;
-                wf_stg(h, out[0][s], ok && i == REAL - 1);
-                wf_stg(h + 1, out[1][s], ok && i == REAL - 1);
+                double *h = ok && i == REAL - 1 ? ho + (int64_t)(tau + SO) * HO + hoff : B.hsink;
+                h[0] = out[0][s];
+                h[1] = out[1][s];
             }
             wf_sts(&wf_xw(B, FP, ib, tau), xo[s] + md[s + 1], ok && real);
         }
@@ -484,6 +486,7 @@ __global__ void __launch_bounds__(wf::NTHREADS, 1) k_wavefront(const __grid_cons
 
     const int n1 = P.n1, b = B.b;
     double *const ho_out = b + 1 < P.nb ? P.ho + (int64_t)b * P.nslot * HO : nullptr;
+    B.hsink = P.ho + ((int64_t)b * P.nslot + P.nslot - 2 * CW) * HO;
     const double *const ho_in = b > 0 ? P.ho + (int64_t)(b - 1) * P.nslot * HO : nullptr;
     // chain state and interior coefficients (negated N, then 1/n_diag)
     WfChain S;
@@ -733,7 +736,7 @@ struct P1Wavefront {
         c1 = (n1 + 2 * (REAL - 1) + OFF_WR + CW) / CW + 1;
         // hand-off slots: written from CW c0 - OFF_C2 on, read up to
         // CW c1 - OFF_G1 - 2 + CW + SKEW
-        nslot = CW * (c1 + 1) - OFF_G1 + SKEW + SO + CW;
+        nslot = CW * (c1 + 1) - OFF_G1 + SKEW + SO + CW + 2 * CW;  // + the dummy slots
         OCMG_REQUIRE(CW * c0 - OFF_C2 + SO >= 0, "hand-off offset too small");
         int dev = 0, sms = 0, coop = 0;
         OCMG_CUDA(cudaGetDevice(&dev));

@@ -73,6 +73,7 @@ __global__ void k(long long *out, double *sink, int iters, int n1) {
     B.n1 = n1;
     B.iy0 = 100;
     B.nreal = 29;
+    B.hsink = sink + (1 << 19);
     WfChain S;
     for (int m = 0; m < 7; ++m) S.acc[m] = 0.0;
     S.pprev = S.v1prev = 0.0;
