@@ -537,12 +537,20 @@ __global__ void __launch_bounds__(wf::NTHREADS, 1) k_wavefront(const __grid_cons
                 P.prof + (((int64_t)blockIdx.x * (P.c1 - P.c0) + (c - P.c0)) * NWARPS + warp) * 3;
             const long long ce = clock64();
             pp[0] = t_begin;
-            pp[1] = (unsigned long long)((t_mid ? t_mid : ce) - c_begin);
+            pp[1] = warp == 8 ? (unsigned long long)t_mid
+                              : (unsigned long long)((t_mid ? t_mid : ce) - c_begin);
             pp[2] = (unsigned long long)(ce - c_begin);
         }
 #endif
         asm volatile("bar.sync 0, %0;" ::"n"(NTHREADS) : "memory");
-        if (threadIdx.x == 0) wfd::st_release(P.iter + b * FLAG_STRIDE, c - P.c0 + 1);
+        if (threadIdx.x == 0) {
+            wfd::st_release(P.iter + b * FLAG_STRIDE, c - P.c0 + 1);
+#ifdef OCMG_WF_PROFILE
+            if (P.prof)  // warp 0's mid slot: when this release was issued (ns)
+                P.prof[(((int64_t)blockIdx.x * (P.c1 - P.c0) + (c - P.c0)) * NWARPS) * 3 + 1] =
+                    gtimer();
+#endif
+        }
     };
 
     if (warp < 2) {
@@ -674,11 +682,13 @@ __global__ void __launch_bounds__(wf::NTHREADS, 1) k_wavefront(const __grid_cons
                     // a schedule bug would spin forever: trap after ~10 s instead
                     unsigned spins = 0;
                     const int need = min(c + DOWN, P.c1 - 1) - P.c0 + 1;
-                    while (wfd::ld_relaxed(P.iter + (b - 1) * FLAG_STRIDE) < need) {
-                        __nanosleep(64);
-                        if (++spins > (1u << 27)) __trap();
-                    }
+                    // a busy poll (one L2 round trip per try)
+                    while (wfd::ld_relaxed(P.iter + (b - 1) * FLAG_STRIDE) < need)
+                        if (++spins > (1u << 25)) __trap();
                     wfd::fence_acq_rel();
+#ifdef OCMG_WF_PROFILE
+                    t_mid = (long long)gtimer();  // scout: poll success (ns)
+#endif
                 }
                 __syncwarp();
                 // 64 values: lane -> (kind, slot); kind 0/1 p1 rows -2/-1 for

@@ -26,6 +26,8 @@ _lib.check(fn(s.handle, buf.ctypes.data_as(ctypes.c_void_p), dims))
 t = buf.reshape(nb, niter, nw, 3).astype(np.int64)
 t0 = t[..., 0][t[..., 0] > 0].min()
 t[..., 0] -= t0
+t[:, :, 0, 1] -= t0
+t[:, :, 8, 1] = np.where(t[:, :, 8, 1] > 0, t[:, :, 8, 1] - t0, 0)
 names = ["chain1", "chain2", "G1", "u", "G2", "r", "loader", "writer", "scout"]
 print(f"k={k} nb={nb} niter={niter} total {(t.max())/1e3:.1f} us")
 for b in (0, nb // 2, nb - 1):
@@ -58,3 +60,18 @@ print("start(b, c+1) - start(b-1, c+DOWN+1) us: median %.2f p10 %.2f p90 %.2f" %
       (np.median(gaps) / 1e3, np.percentile(gaps, 10) / 1e3, np.percentile(gaps, 90) / 1e3))
 per = np.diff(t[:, :, 0, 0], axis=1)
 print("iteration period us: median %.2f p90 %.2f" % (np.median(per) / 1e3, np.percentile(per, 90) / 1e3))
+# flag hand-off: band b's scout saw band b-1's counter (need = c + DOWN + 1
+# iterations done) at scout[c][1]; band b-1 issued that release at
+# chain1[c + DOWN][1] (warp 0's mid slot holds the release time in ns)
+lat = []
+for b in range(1, nb):
+    for c in range(20, niter - DOWN - 2):
+        seen = t[b, c, 8, 1]
+        rel = t[b - 1, c + DOWN, 0, 1]
+        if seen > 0 and rel > 0:
+            lat.append(int(seen) - int(rel))
+lat = np.array(lat)
+if lat.size:
+    print("release -> seen by the band below (ns): median %d p10 %d p90 %d; "
+          "negative = seen before the release time was stamped" %
+          (np.median(lat), np.percentile(lat, 10), np.percentile(lat, 90)))
