@@ -535,7 +535,11 @@ void level_ne_gs(const ocmg_level *lv, int mode, bool forward, double *x,
             else
                 OCMG_LAUNCH(k_p1_gs_small<false>, 1, nt, gs_small_smem(n1), s, n1, lv->tables.p,
                             forward ? 1 : 0, x, r);
-        } else if (n1 >= gsd::kMinN1 && n1 <= gsd::kMaxN1) {
+        } else if (n1 >= gsd::kMinN1 && n1 <= gsd::kMaxN1 &&
+                   !(mode == OCMG_GS_WAVEFRONT && lv->wf.ready())) {
+            // (the wavefront mode takes the band kernel from L7 up: 5-9
+            // bands run a sweep in ~0.1-0.2 ms against the one-CTA ring's
+            // 0.23-0.57 ms; the reference mode keeps the bitwise ring)
             // both exact modes: one CTA, anti-diagonal ring of r
             const int nt = 2 * gsd::per_field(n1);
             const size_t sm = gsd::smem(n1);
