@@ -451,7 +451,8 @@ def run_strip_arm(args, ws, rank, local):
         rh.copy_(rs[1], non_blocking=True)
     t_e2e = max_over_ranks(time_events(e2e_step, max(1, args.steps), stream),
                            ws, device)
-    # config 3 on the partition: W(2,2) multicolour cycle, coarsest L3
+    # config 3 on the partition: W(2,2) multicolour cycle, coarsest L1 (the
+    # reference default; the partition needs a gathered smoothed level)
     from paper_1502_03917_b200.strips import (DistComm, LoopbackComm,
                                               StripMultigrid)
     solve = None
@@ -459,7 +460,7 @@ def run_strip_arm(args, ws, rank, local):
     if not args.no_solve_l12:
         del rs, xo
         cfg = P.CycleConfig(smoother=P.SmootherKind("lsgs"), cycle="w",
-                            coarsest_level=3, gs_mode="multicolour")
+                            coarsest_level=1, gs_mode="multicolour")
         mg = P.build_solver("poisson", args.level, args.alpha, cfg)
         fs = P.baseline_rhs(mg.finest, 0, add_sine=True)
         sm = StripMultigrid(mg, ws, [rank], DistComm() if ws > 1 else LoopbackComm())
@@ -471,7 +472,7 @@ def run_strip_arm(args, ws, rank, local):
         torch.cuda.synchronize()
         t_solve = max_over_ranks(time.perf_counter() - t0, ws, device)
         solve = {"config": f"poisson L{args.level} alpha={args.alpha} W(2,2) "
-                           "NE-GS[multicolour] coarsest L3 y_D=U+sin*sin, "
+                           "NE-GS[multicolour] coarsest L1 y_D=U+sin*sin, "
                            f"row strips x{ws} (levels >= "
                            f"{mg.systems[sm.first].level} partitioned)",
                  "cycles": len(hist), "final_rel_residual": hist[-1],

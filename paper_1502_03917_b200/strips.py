@@ -338,14 +338,17 @@ class StripMultigrid:
         cfg = mg.config
         if cfg.gs_mode != "multicolour" or cfg.smoother.name not in ("lsgs", "slsgs"):
             raise ValueError("strip cycles run multicolour NE-GS smoothers")
-        if not all(getattr(s, "structured", False) for s in mg.systems[1:]):
-            raise ValueError("strip cycles need structured Poisson levels")
         self.mg, self.comm = mg, comm
         n1s = [2 ** s.level + 1 for s in mg.systems]
         first, bounds = nested_bounds(n1s, world_size)
         if first < 2:
             raise ValueError("partitioned levels must leave a gathered "
                              "sub-hierarchy of at least one smoothed level")
+        # partitioned levels and the gathered one they restrict into are
+        # structured; below that any level kind runs (the gathered
+        # sub-cycle is the single-GPU ocmg_cycle)
+        if not all(getattr(s, "structured", False) for s in mg.systems[first - 1:]):
+            raise ValueError("strip cycles need structured Poisson levels")
         self.first, self.gather = first, first - 1
         # each rank restricts the gathered level's rows that its fine strip
         # covers: coarse row c reads fine rows 2c-1 .. 2c+1 (one ghost row)

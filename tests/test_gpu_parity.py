@@ -638,3 +638,24 @@ def test_fixed_point_full_size(mode):
     r2 = dsys.residual(x, f)
     err = float((r - r2).abs().max() / r2.abs().max())
     assert err < 1e-9, err
+
+
+def test_solve_divergence_stop():
+    """The on-device loop stops like Multigrid.solve once the relative
+    residual exceeds DIVERGENCE_FACTOR times its entering value
+    (multigrid.py:26,198-200): with the factor forced tiny, one cycle
+    already counts as divergence."""
+    import ctypes
+    cfg = P.CycleConfig(smoother=P.SmootherKind("lsgs"), cycle="v")
+    mg = P.build_solver("poisson", 5, 1e-6, cfg)
+    f = P.baseline_rhs(mg.finest, 0)
+    x = torch.zeros_like(f)
+    hist = np.zeros(10)
+    done, div = ctypes.c_int(), ctypes.c_int()
+    _lib.call("ocmg_solve_ex", mg.native().handle, _lib.dptr(x), _lib.dptr(f),
+              1e-8, 10, 1, 1e-30, _lib.hptr(hist), ctypes.byref(done),
+              ctypes.byref(div), _lib.stream_ptr())
+    assert div.value == 1 and done.value == 1
+    # the default factor (1e6) never fires on a converging solve
+    _, h = mg.solve_to_tolerance(f, tol=1e-8, max_cycles=60)
+    assert not mg.last_diverged and h[-1] <= 1e-8

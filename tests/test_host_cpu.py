@@ -173,3 +173,27 @@ def test_config_validation():
         P.CycleConfig(smoother=P.SmootherKind("lsgs"), nu_pre=0, nu_post=0)
     with pytest.raises(ValueError):
         P.CycleConfig(smoother=P.SmootherKind("lsgs"), gs_mode="fast")
+
+
+def test_table_request_and_renderers():
+    """The table runner's request normalisation and its three formats
+    (no GPU: cells filled by hand)."""
+    from paper_1502_03917_b200 import tables as T
+    with pytest.raises(ValueError):
+        T.TableRequest(problem="heat").resolved()
+    with pytest.raises(ValueError):
+        T.TableRequest(problem="poisson", levels=(1, 2)).resolved()
+    req = T.TableRequest(problem="poisson", smoothers=("lsgs",), levels=(3, 4),
+                         alphas=(1.0,)).resolved()
+    assert req.steps("slsgs") == (1, 1) and req.steps("lsgs") == (2, 2)
+    tab = T.IterationTable(req)
+    tab.add(T.TableCell("lsgs", 1.0, 3, 11, True))
+    tab.add(T.TableCell("lsgs", 1.0, 4, None, False, "boom"))
+    md = tab.render("markdown")
+    assert "| level | lsgs a=1 |" in md and "| 3 | 11 |" in md and "| 4 | div |" in md
+    csv_ = tab.render("csv").splitlines()
+    assert csv_[0] == "problem,smoother,alpha,level,iterations,converged"
+    assert csv_[2] == "poisson,lsgs,1,4,,false"
+    import json
+    js = json.loads(tab.render("json"))
+    assert js["cells"][0]["iterations"] == 11 and js["cells"][1]["converged"] is False
