@@ -162,6 +162,15 @@ int ocmg_restrict_rows(const ocmg_transfer *t, const double *rf, double *rc,
                        int cy_begin, int cy_end, void *stream);
 int ocmg_prolong_add_rows(const ocmg_transfer *t, const double *c, double *xf,
                           int fy_begin, int fy_end, void *stream);
+/* The two halves of an NE-Jacobi sweep (kernels.normal_sweep, kernels.py:
+ * 27-32 and 33-38) on the rows [y_begin, y_end) of a structured P1 level,
+ * for a strip: p = tau W r / L needs r of rows y_begin-1 .. y_end; the apply
+ * half (x += p, r -= A p) needs p of rows y_begin-1 .. y_end.  Full-size
+ * vectors; the arithmetic of ocmg_ne_jacobi_sweep row for row. */
+int ocmg_ne_jacobi_p_rows(const ocmg_level *lv, double tau, const double *r, double *p,
+                          int y_begin, int y_end, void *stream);
+int ocmg_ne_jacobi_apply_rows(const ocmg_level *lv, const double *p, double *x, double *r,
+                              int y_begin, int y_end, void *stream);
 
 /* One collective Gauss-Seidel sweep over state/adjoint vertex pairs
  * (kernels.collective_sweep, kernels.py:70-96, via cgs_sweep,

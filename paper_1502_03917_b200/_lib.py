@@ -76,6 +76,8 @@ SIGNATURES = {
     "ocmg_level_set_vanka": (_I, [_P, _I64, _I, _P, _P, _P]),
     "ocmg_vanka_sweep": (_I, [_P, _D, _I, _P, _P, _P, ctypes.POINTER(_I64)]),
     "ocmg_restrict_rows": (_I, [_P, _P, _P, _I, _I, _P]),
+    "ocmg_ne_jacobi_p_rows": (_I, [_P, _D, _P, _P, _I, _I, _P]),
+    "ocmg_ne_jacobi_apply_rows": (_I, [_P, _P, _P, _P, _I, _I, _P]),
     "ocmg_prolong_add_rows": (_I, [_P, _P, _P, _I, _I, _P]),
     "ocmg_mean_project": (_I, [_P, _P, _P]),
     "ocmg_norm2": (_I, [_P, _P, _I, _P, _P]),

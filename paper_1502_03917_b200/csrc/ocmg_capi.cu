@@ -334,23 +334,35 @@ void level_residual(const ocmg_level *lv, const double *x, const double *f,
     OCMG_LAUNCH_CHECK();
 }
 
+// the two halves of an NE-Jacobi sweep on a structured level, for the rows
+// [ylo, yhi) (a strip: p of rows ylo..yhi needs r of rows ylo-1..yhi, the
+// apply half p of rows ylo-1..yhi)
+void p1_ne_p_half(const ocmg_level *lv, double tau, const double *r, double *p,
+                  cudaStream_t s, int ylo, int yhi) {
+    const dim3 g = p1_interior_grid(lv->n1), b(kTX, kTY);
+    P1JacCoef C;
+    for (int t = 0; t < 28; ++t) C.w[t] = lv->cW.c[t];
+    C.l[0] = lv->cL[0];
+    C.l[1] = lv->cL[1];
+    C.tau = tau;
+    OCMG_LAUNCH(k_p1_ne_p_int, g, b, 0, s, lv->n1, C, r, p, ylo, yhi);
+    OCMG_LAUNCH(k_p1_ne_p_ring, grid_for(p1_ring_count(lv->n1, kRing), kBlk), kBlk, 0, s,
+                lv->n1, lv->tables.p, tau, r, p, ylo, yhi);
+}
+void p1_ne_apply_half(const ocmg_level *lv, const double *p, double *x, double *r,
+                      cudaStream_t s, int ylo, int yhi) {
+    const dim3 g = p1_interior_grid(lv->n1), b(kTX, kTY);
+    const dim3 ga(g.x, (lv->n1 - 2 * kRing + kTY * (kRPT / 2) - 1) / (kTY * (kRPT / 2)));
+    OCMG_LAUNCH(k_p1_ne_apply_int, ga, b, 0, s, lv->n1, lv->cA, p, x, r, ylo, yhi);
+    OCMG_LAUNCH(k_p1_ne_apply_ring, grid_for(p1_ring_count(lv->n1, kRing), kBlk), kBlk, 0,
+                s, lv->n1, lv->tables.p, p, x, r, ylo, yhi);
+}
+
 void level_ne_jacobi(const ocmg_level *lv, double tau, double *x, double *r,
                      double *scratch, cudaStream_t s) {
     if (lv->kind == kP1) {
-        const dim3 g = p1_interior_grid(lv->n1), b(kTX, kTY);
-        const int64_t nring = p1_ring_count(lv->n1, kRing);
-        P1JacCoef C;
-        for (int t = 0; t < 28; ++t) C.w[t] = lv->cW.c[t];
-        C.l[0] = lv->cL[0];
-        C.l[1] = lv->cL[1];
-        C.tau = tau;
-        OCMG_LAUNCH(k_p1_ne_p_int, g, b, 0, s, lv->n1, C, r, scratch);
-        OCMG_LAUNCH(k_p1_ne_p_ring, grid_for(nring, kBlk), kBlk, 0, s, lv->n1,
-                    lv->tables.p, tau, r, scratch);
-        const dim3 ga(g.x, (lv->n1 - 2 * kRing + kTY * (kRPT / 2) - 1) / (kTY * (kRPT / 2)));
-        OCMG_LAUNCH(k_p1_ne_apply_int, ga, b, 0, s, lv->n1, lv->cA, scratch, x, r);
-        OCMG_LAUNCH(k_p1_ne_apply_ring, grid_for(nring, kBlk), kBlk, 0, s, lv->n1,
-                    lv->tables.p, scratch, x, r);
+        p1_ne_p_half(lv, tau, r, scratch, s, 0, lv->n1);
+        p1_ne_apply_half(lv, scratch, x, r, s, 0, lv->n1);
     } else {
         const SellDev &S = lv->sell;
         OCMG_LAUNCH(k_sell_ne_p, grid_for(lv->n, kBlk), kBlk, 0, s, lv->n, S.base.p,
@@ -1471,6 +1483,29 @@ int ocmg_residual_rows(const ocmg_level *lv, const double *x, const double *f,
         OCMG_REQUIRE(lv->kind == kP1, "row ranges need a structured P1 level");
         OCMG_REQUIRE(0 <= y_begin && y_begin <= y_end && y_end <= lv->n1, "bad rows");
         level_residual(lv, x, f, r, as_stream(stream), y_begin, y_end);
+    });
+}
+
+int ocmg_ne_jacobi_p_rows(const ocmg_level *lv, double tau, const double *r, double *p,
+                          int y_begin, int y_end, void *stream) {
+    return guarded([&] {
+        OCMG_REQUIRE(lv && r && p, "null argument");
+        OCMG_REQUIRE(lv->kind == kP1, "row ranges need a structured P1 level");
+        OCMG_REQUIRE(tau > 0.0 && tau < 2.0, "damping parameter must lie in (0, 2)");
+        OCMG_REQUIRE(0 <= y_begin && y_begin <= y_end && y_end <= lv->n1, "bad rows");
+        p1_ne_p_half(lv, tau, r, p, as_stream(stream), y_begin, y_end);
+        OCMG_LAUNCH_CHECK();
+    });
+}
+
+int ocmg_ne_jacobi_apply_rows(const ocmg_level *lv, const double *p, double *x, double *r,
+                              int y_begin, int y_end, void *stream) {
+    return guarded([&] {
+        OCMG_REQUIRE(lv && p && x && r, "null argument");
+        OCMG_REQUIRE(lv->kind == kP1, "row ranges need a structured P1 level");
+        OCMG_REQUIRE(0 <= y_begin && y_begin <= y_end && y_end <= lv->n1, "bad rows");
+        p1_ne_apply_half(lv, p, x, r, as_stream(stream), y_begin, y_end);
+        OCMG_LAUNCH_CHECK();
     });
 }
 

@@ -220,12 +220,14 @@ __device__ __forceinline__ void p1_nep_rows(const P1JacCoef &C, int64_t N, int n
 
 __global__ void __launch_bounds__(kTX *kTY, 4)
     k_p1_ne_p_int(int n1, const __grid_constant__ P1JacCoef C,
-                  const double *__restrict__ r, double *__restrict__ p) {
+                  const double *__restrict__ r, double *__restrict__ p, int ylo, int yhi) {
+    // interior columns and rows, restricted to the rows [ylo, yhi)
     const int lo = kRing, hi = n1 - 1 - kRing;
+    const int rlo = max(lo, ylo), rhi = min(hi, yhi - 1);
     const int ix = lo + blockIdx.x * kTX + threadIdx.x;
-    const int iy0 = lo + (blockIdx.y * kTY + threadIdx.y) * kRPT;
-    if (ix > hi || iy0 > hi) return;
-    const int nrows = min(kRPT, hi - iy0 + 1);
+    const int iy0 = rlo + (blockIdx.y * kTY + threadIdx.y) * kRPT;
+    if (ix > hi || iy0 > rhi) return;
+    const int nrows = min(kRPT, rhi - iy0 + 1);
     const int64_t N = (int64_t)n1 * n1, v0 = (int64_t)iy0 * n1 + ix;
     if (nrows == kRPT)
         p1_nep_rows<kRPT>(C, N, n1, v0, r, p, nrows);
@@ -235,10 +237,10 @@ __global__ void __launch_bounds__(kTX *kTY, 4)
 
 __global__ void k_p1_ne_p_ring(int n1, const double *__restrict__ T, double tau,
                                const double *__restrict__ r,
-                               double *__restrict__ p) {
+                               double *__restrict__ p, int ylo, int yhi) {
     int ix, iy;
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (!p1_ring_node(k, n1, kRing, ix, iy)) return;
+    if (!p1_ring_node(k, n1, kRing, ix, iy) || iy < ylo || iy >= yhi) return;
     const int64_t N = (int64_t)n1 * n1;
     const P1Node q = p1_node(ix, iy, n1);
     const double *W = T + kP1OffW + q.c * 28;
@@ -311,14 +313,15 @@ __device__ __forceinline__ void p1_neapply_rows(const P1Coef28 &A, int64_t N,
 __global__ void __launch_bounds__(kTX *kTY, 3)
     k_p1_ne_apply_int(int n1, const __grid_constant__ P1Coef28 A,
                       const double *__restrict__ p, double *__restrict__ x,
-                      double *__restrict__ r) {
+                      double *__restrict__ r, int ylo, int yhi) {
     // 4 rows per thread here: the x/r preload of 8 rows cost occupancy
     constexpr int R = kRPT / 2;
     const int lo = kRing, hi = n1 - 1 - kRing;
+    const int rlo = max(lo, ylo), rhi = min(hi, yhi - 1);
     const int ix = lo + blockIdx.x * kTX + threadIdx.x;
-    const int iy0 = lo + (blockIdx.y * kTY + threadIdx.y) * R;
-    if (ix > hi || iy0 > hi) return;
-    const int nrows = min(R, hi - iy0 + 1);
+    const int iy0 = rlo + (blockIdx.y * kTY + threadIdx.y) * R;
+    if (ix > hi || iy0 > rhi) return;
+    const int nrows = min(R, rhi - iy0 + 1);
     const int64_t N = (int64_t)n1 * n1, v0 = (int64_t)iy0 * n1 + ix;
     if (nrows == R)
         p1_neapply_rows<R, true>(A, N, n1, v0, p, x, r, nrows);
@@ -329,10 +332,10 @@ __global__ void __launch_bounds__(kTX *kTY, 3)
 __global__ void k_p1_ne_apply_ring(int n1, const double *__restrict__ T,
                                    const double *__restrict__ p,
                                    double *__restrict__ x,
-                                   double *__restrict__ r) {
+                                   double *__restrict__ r, int ylo, int yhi) {
     int ix, iy;
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (!p1_ring_node(k, n1, kRing, ix, iy)) return;
+    if (!p1_ring_node(k, n1, kRing, ix, iy) || iy < ylo || iy >= yhi) return;
     const int64_t N = (int64_t)n1 * n1;
     const P1Node q = p1_node(ix, iy, n1);
     const double *A = T + kP1OffA + q.c * 28;

@@ -336,8 +336,12 @@ class StripMultigrid:
 
     def __init__(self, mg, world_size, ranks, comm):
         cfg = mg.config
-        if cfg.gs_mode != "multicolour" or cfg.smoother.name not in ("lsgs", "slsgs"):
-            raise ValueError("strip cycles run multicolour NE-GS smoothers")
+        self.jacobi = cfg.smoother.name == "normal"
+        if not self.jacobi and (cfg.gs_mode != "multicolour" or
+                                cfg.smoother.name not in ("lsgs", "slsgs")):
+            raise ValueError("strip cycles run multicolour NE-GS or NE-Jacobi "
+                             "smoothers")
+        self.tau = cfg.smoother.tau
         self.mg, self.comm = mg, comm
         n1s = [2 ** s.level + 1 for s in mg.systems]
         first, bounds = nested_bounds(n1s, world_size)
@@ -381,8 +385,29 @@ class StripMultigrid:
                       _lib.dptr(st.r2[i]), _lib.stream_ptr(), ctypes.byref(ops))
             st.r[i], st.r2[i] = st.r2[i], st.r[i]
 
+    def _jacobi(self, i):
+        """NE-Jacobi on the strips (kernels.py:17-39): r ghost (1 row) -> p
+        of the own rows -> p ghost (1 row) -> x += p, r -= A p on the own
+        rows; the arithmetic of the single-GPU halves row for row."""
+        sysi = self.mg.systems[i]
+        self.comm.exchange(self.states, i, "r", 1)
+        for st in self.states:
+            y0, y1 = st.bounds[i]
+            _lib.call("ocmg_ne_jacobi_p_rows", sysi.handle, float(self.tau),
+                      _lib.dptr(st.r[i]), _lib.dptr(st.r2[i]), y0, y1,
+                      _lib.stream_ptr())
+        self.comm.exchange(self.states, i, "r2", 1)
+        for st in self.states:
+            y0, y1 = st.bounds[i]
+            _lib.call("ocmg_ne_jacobi_apply_rows", sysi.handle, _lib.dptr(st.r2[i]),
+                      _lib.dptr(st.x[i]), _lib.dptr(st.r[i]), y0, y1,
+                      _lib.stream_ptr())
+
     def _smooth(self, i, nu):
         for _ in range(nu):
+            if self.jacobi:
+                self._jacobi(i)
+                continue
             self._sweep(i, True)
             if self.slsgs:
                 self._sweep(i, False)

@@ -367,16 +367,23 @@ def test_fused_coarse_block_is_bit_identical(cycle, smoother, k, coarsest):
     assert hs[0] == hs[1]
 
 
-@pytest.mark.parametrize("k,ws,cycle,smoother", [(8, 2, "v", "lsgs"),
-                                                  (9, 4, "w", "lsgs"),
-                                                  (9, 3, "v", "slsgs")])
-def test_strip_multigrid_matches_single_gpu(k, ws, cycle, smoother):
+@pytest.mark.parametrize("k,ws,cycle,smoother,co", [(8, 2, "v", "lsgs", 3),
+                                                     (9, 4, "w", "lsgs", 3),
+                                                     (9, 3, "v", "slsgs", 3),
+                                                     (9, 2, "w", "lsgs", 1),
+                                                     (9, 3, "v", "normal", 3),
+                                                     (10, 4, "w", "normal", 1)])
+def test_strip_multigrid_matches_single_gpu(k, ws, cycle, smoother, co):
     """The strip-partitioned cycle, every rank run in this
     process with loopback exchanges, reproduces the single-GPU cycle bit for
-    bit; the stopping norms agree to rounding."""
+    bit -- multicolour NE-GS (15 ghost rows per sweep) and NE-Jacobi (r and
+    p ghost rows, one each), down to the reference's coarsest level L1; the
+    stopping norms agree to rounding."""
     from paper_1502_03917_b200.strips import LoopbackComm, StripMultigrid
-    cfg = P.CycleConfig(smoother=P.SmootherKind(smoother), cycle=cycle,
-                        coarsest_level=3, gs_mode="multicolour")
+    kind = (P.SmootherKind("normal", tau=0.4) if smoother == "normal"
+            else P.SmootherKind(smoother))
+    cfg = P.CycleConfig(smoother=kind, cycle=cycle, coarsest_level=co,
+                        gs_mode="multicolour")
     mg = P.build_solver("poisson", k, 1e-6, cfg)
     f = P.baseline_rhs(mg.finest, 0, add_sine=True)
     x1, h1 = mg.solve_to_tolerance(f, tol=0.0, max_cycles=3)
