@@ -259,6 +259,20 @@ int ocmg_hierarchy_destroy(ocmg_hierarchy *h);
 /* One cycle on the finest level: x <- cycle(x, f) (multigrid.py:130-159)
  * followed by nothing else.  x, f: finest-level device vectors. */
 int ocmg_cycle(ocmg_hierarchy *h, double *x, const double *f, void *stream);
+/* The coarse correction of hierarchy index level_index (1..n_levels) for
+ * the restricted residual crhs (its coarse level's length): corr = rec
+ * cycles of index level_index - 1 from zero (rec = 2 for a W-cycle above
+ * the coarse solve, multigrid.py:150-152).  Outside the reference mode the
+ * library collapses that map for the coarse end of the hierarchy (levels of
+ * at most 2304 unknowns below the finest) into one dense matrix built at
+ * ocmg_hierarchy_create from the same device cycle on unit vectors; this
+ * call applies whichever form the cycle uses (partitioned cycles call it to
+ * stay bit-identical to ocmg_cycle). */
+int ocmg_coarse_correction(ocmg_hierarchy *h, int level_index, const double *crhs,
+                           double *corr, void *stream);
+/* *level_index = the hierarchy index c whose visits the cycle has collapsed
+ * into the coarse correction of index c + 1 (0: none). */
+int ocmg_hierarchy_collapsed_level(const ocmg_hierarchy *h, int *level_index);
 /* BASELINE protocol loop: repeat { cycle; mean projection; rel =
  * ||f-Ax||_2/||f||_2 } until rel <= tol or max_cycles.  hist (host,
  * max_cycles doubles) receives rel per cycle; *n_done the cycle count.

@@ -93,6 +93,8 @@ SIGNATURES = {
                                    ctypes.POINTER(CycleConfigC), _PP]),
     "ocmg_hierarchy_destroy": (_I, [_P]),
     "ocmg_cycle": (_I, [_P, _P, _P, _P]),
+    "ocmg_coarse_correction": (_I, [_P, _I, _P, _P, _P]),
+    "ocmg_hierarchy_collapsed_level": (_I, [_P, _P]),
     "ocmg_solve": (_I, [_P, _P, _P, _D, _I, _I, _P, ctypes.POINTER(_I),
                         _P]),
     "ocmg_solve_ex": (_I, [_P, _P, _P, _D, _I, _I, _D, _P,

@@ -17,6 +17,7 @@
 #include "ocmg_p1_mc.cuh"
 #include "ocmg_p1_mc_small.cuh"
 #include "ocmg_p1_gsdiag.cuh"
+#include "ocmg_p1_dense.cuh"
 #include "ocmg_subcycle.cuh"
 #include "ocmg_cgs.cuh"
 #include "ocmg_cgs_mc.cuh"
@@ -91,6 +92,10 @@ struct ocmg_level {
     P1Coef28 cA{}, cW{};  // class-(3,3) A and row_scaled rows (tiled kernels)
     double cL[2] = {0.0, 0.0};
     P1Wavefront wf;
+    // k <= 5: the exact-order sweep as a dense map (ocmg_p1_dense.cuh), S
+    // row-major per direction, and its scratch d = S r
+    DevBuf<double> pmap[2], pmap_d;
+    bool has_pmap = false;
     int mc_tier = 2;          // 0 one-CTA, 1 cooperative, 2 pipelined strips
     int mc_grid = 0;          // tier-1 CTAs
     DevBuf<unsigned> mc_bar;  // tier-1 grid barrier
@@ -135,6 +140,13 @@ struct ocmg_hierarchy {
     int sub_hi = 0;
     SubcycleParams sub{};
     size_t sub_smem = 0;
+    // collapsed coarse end (setup_collapse): the coarse correction of
+    // hierarchy index col_hi + 1, i.e. its rec visits of index col_hi from a
+    // zero start, is the dense map col_map (row-major, leading dimension
+    // col_ld) applied to the restricted residual (0 = off)
+    int col_hi = 0, col_ld = 0;
+    DevBuf<double> col_map;
+    int64_t col_max_n = 0;
     cudaGraphExec_t graph = nullptr;
     const double *graph_x = nullptr, *graph_f = nullptr;
     cudaStream_t graph_stream = nullptr;
@@ -538,15 +550,23 @@ void level_ne_gs(const ocmg_level *lv, int mode, bool forward, double *x,
             if (p1_mc_sweep(lv, forward, x, r, lv->mc_r.p, s))
                 OCMG_CUDA(cudaMemcpyAsync(r, lv->mc_r.p, sizeof(double) * lv->n,
                                           cudaMemcpyDeviceToDevice, s));
+        } else if (mode == OCMG_GS_WAVEFRONT && lv->has_pmap) {
+            // k <= 5: d = S r, then x += d, r -= A d
+            const int n = (int)lv->n;
+            OCMG_LAUNCH(k_dense_rows, (n + kDenseRowsWarps - 1) / kDenseRowsWarps,
+                        32 * kDenseRowsWarps, 0, s, n, n, lv->pmap[forward ? 0 : 1].p, r,
+                        lv->pmap_d.p);
+            OCMG_LAUNCH(k_p1_dense_finish, grid_for(n / 2, 128), 128, 0, s, n1, lv->tables.p,
+                        lv->pmap_d.p, x, r);
         } else if (n1 <= kGsSmallMaxN1 && ((uintptr_t)x % 16 | (uintptr_t)r % 16) == 0) {
             // both exact modes: one CTA, levels separated by barriers
             const int nt = 64 * ((n1 + 1) / 2 > 32 ? 2 : 1);
             if (mode == OCMG_GS_WAVEFRONT)
                 OCMG_LAUNCH(k_p1_gs_small<true>, 1, nt, gs_small_smem(n1), s, n1, lv->tables.p,
-                            forward ? 1 : 0, x, r);
+                            forward ? 1 : 0, x, r, (int64_t)0);
             else
                 OCMG_LAUNCH(k_p1_gs_small<false>, 1, nt, gs_small_smem(n1), s, n1, lv->tables.p,
-                            forward ? 1 : 0, x, r);
+                            forward ? 1 : 0, x, r, (int64_t)0);
         } else if (n1 >= gsd::kMinN1 && n1 <= gsd::kMaxN1 &&
                    !(mode == OCMG_GS_WAVEFRONT && lv->wf.ready())) {
             // (the wavefront mode takes the band kernel from L7 up: 5-9
@@ -936,6 +956,28 @@ void smooth_n(ocmg_hierarchy *h, int hi, int nu, double *x, double *r,
 }
 
 void cycle_rec(ocmg_hierarchy *h, int hi, double *x, const double *rhs,
+               cudaStream_t s);
+
+// corr = the coarse correction of hierarchy index hi for the restricted
+// residual crhs: rec visits of index hi - 1 from zero (multigrid.py:150-152),
+// or, collapsed (setup_collapse), G crhs in one launch
+void coarse_correction(ocmg_hierarchy *h, int hi, const double *crhs, double *corr,
+                       cudaStream_t s) {
+    const int64_t nc = h->corr[hi - 1].n;
+    if (h->col_hi > 0 && hi - 1 == h->col_hi) {
+        OCMG_LAUNCH(k_dense_rows, (unsigned)((nc + kDenseRowsWarps - 1) / kDenseRowsWarps),
+                    32 * kDenseRowsWarps, 0, s, (int)nc, h->col_ld, h->col_map.p, crhs, corr);
+        OCMG_LAUNCH_CHECK();
+        return;
+    }
+    OCMG_CUDA(cudaMemsetAsync(corr, 0, nc * sizeof(double), s));
+    // the exact coarse solve ignores its start vector, so the W-cycle's
+    // second visit of level 0 would recompute the same vector: elided
+    const int rec = (h->cfg.cycle_w && hi - 1 > 0) ? 2 : 1;
+    for (int k = 0; k < rec; ++k) cycle_rec(h, hi - 1, corr, crhs, s);
+}
+
+void cycle_rec(ocmg_hierarchy *h, int hi, double *x, const double *rhs,
                cudaStream_t s) {
     if (h->sub_hi > 0 && hi == h->sub_hi) {
         SubcycleParams P = h->sub;
@@ -959,16 +1001,68 @@ void cycle_rec(ocmg_hierarchy *h, int hi, double *x, const double *rhs,
     smooth_n(h, hi, h->cfg.nu_pre, x, r, s);
     double *crhs = h->crhs[hi - 1].p, *corr = h->corr[hi - 1].p;
     do_restrict(tr, r, crhs, s);
-    const int64_t nc = h->corr[hi - 1].n;
-    OCMG_CUDA(cudaMemsetAsync(corr, 0, nc * sizeof(double), s));
-    // the exact coarse solve ignores its start vector, so the W-cycle's
-    // second visit of level 0 would recompute the same vector: elided
-    const int rec = (h->cfg.cycle_w && hi - 1 > 0) ? 2 : 1;
-    for (int k = 0; k < rec; ++k) cycle_rec(h, hi - 1, corr, crhs, s);
+    coarse_correction(h, hi, crhs, corr, s);
     do_prolong_add(tr, corr, x, s);
     level_mean_project(lv, x, s);
     level_residual(lv, x, rhs, r, s);
     smooth_n(h, hi, h->cfg.nu_post, x, r, s, true);
+}
+
+// Collapse the coarse end of the cycle into one dense map.  Every smoother,
+// transfer and the coarse solve are linear, so the coarse correction of
+// hierarchy index c + 1 -- rec visits of index c from a zero start on the
+// restricted residual b (multigrid.py:150-152) -- is corr = G_c b for a fixed
+// matrix G_c.  Its columns are built by running exactly that device code on
+// the unit vectors e_j, bottom up (G_c's own coarse correction uses G_{c-1}),
+// and the deepest index with at most max_n unknowns below the finest level is
+// kept.  In a W-cycle from L12 this replaces the 2^(12-k) visits of every
+// level k <= 5 (~17K launches) by 64 map applications of 38 MB, L2-resident.
+// Not in the reference mode (its contract is bit-identity with the
+// reference's arithmetic); the other modes keep their 1e-12 contract.
+constexpr int64_t kCollapseMaxN = 2304;  // Poisson L5: 2178 unknowns
+
+void setup_collapse(ocmg_hierarchy *h, int64_t max_n) {
+    h->col_hi = 0;
+    h->col_map = DevBuf<double>();
+    h->col_max_n = max_n;
+    h->graph_x = nullptr;  // recapture
+    h->graph_f = nullptr;
+    if (max_n <= 0 || h->cfg.gs_mode == OCMG_GS_REFERENCE) return;
+    const int nl = (int)h->levels.size();
+    int m = 0;
+    for (int c = 1; c < nl; ++c) {  // c < nl: the finest level is never collapsed
+        if (h->levels[c - 1]->n > max_n) break;
+        m = c;
+    }
+    if (m < 1) return;
+    const int saved_sub = h->sub_hi;
+    h->sub_hi = 0;  // per-level path during the build (the fused block's
+                    // single launch is slower than the smaller maps)
+    cudaStream_t s = nullptr;
+    for (int c = 1; c <= m; ++c) {
+        const int64_t n = h->levels[c - 1]->n;
+        const int ld = (int)(n + (n & 1));
+        DevBuf<double> X, G;
+        X.alloc(n * ld);
+        G.alloc(n * ld);
+        double *crhs = h->crhs[c].p, *corr = h->corr[c].p;
+        const int rec = (h->cfg.cycle_w && c > 0) ? 2 : 1;
+        for (int64_t j = 0; j < n; ++j) {
+            OCMG_LAUNCH(k_unit_vector, grid_for(n, kBlk), kBlk, 0, s, n, j, crhs);
+            OCMG_CUDA(cudaMemsetAsync(corr, 0, n * sizeof(double), s));
+            for (int k = 0; k < rec; ++k) cycle_rec(h, c, corr, crhs, s);
+            OCMG_CUDA(cudaMemcpyAsync(X.p + j * ld, corr, n * sizeof(double),
+                                      cudaMemcpyDeviceToDevice, s));
+        }
+        OCMG_LAUNCH(k_dense_transpose, dim3((unsigned)((n + 31) / 32), (unsigned)((n + 31) / 32)),
+                    dim3(32, 8), 0, s, (int)n, ld, X.p, G.p);
+        OCMG_LAUNCH_CHECK();
+        OCMG_CUDA(cudaStreamSynchronize(s));
+        h->col_map = std::move(G);
+        h->col_ld = ld;
+        h->col_hi = c;
+    }
+    h->sub_hi = saved_sub;
 }
 
 // Enable the fused coarse block when the bottom of the hierarchy is
@@ -1256,6 +1350,28 @@ int ocmg_level_create_p1(int k, double alpha, const double *tables,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, gsm));
                 OCMG_CUDA(cudaFuncSetAttribute(k_p1_gs_diag<320, gsd::kRing, true, true>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, gsm));
+            }
+            if (lv->n1 <= kP1DenseMaxN1) {
+                // dense exact-order maps: column j = the reference-order
+                // sweep of unit residual j from x = 0 (one CTA per column)
+                const int n = (int)lv->n;
+                DevBuf<double> X, R;
+                X.alloc((int64_t)n * n);
+                R.alloc((int64_t)n * n);
+                const int nt = 64 * ((lv->n1 + 1) / 2 > 32 ? 2 : 1);
+                for (int dir = 0; dir < 2; ++dir) {
+                    OCMG_LAUNCH(k_p1_dense_unit, grid_for((int64_t)n * n, kBlk), kBlk, 0, 0, n,
+                                X.p, R.p);
+                    OCMG_LAUNCH(k_p1_gs_small<false>, (unsigned)n, nt, gs_small_smem(lv->n1), 0,
+                                lv->n1, lv->tables.p, dir == 0 ? 1 : 0, X.p, R.p, (int64_t)n);
+                    lv->pmap[dir].alloc((int64_t)n * n);
+                    OCMG_LAUNCH(k_dense_transpose, dim3((n + 31) / 32, (n + 31) / 32), dim3(32, 8),
+                                0, 0, n, n, X.p, lv->pmap[dir].p);
+                    OCMG_LAUNCH_CHECK();
+                }
+                OCMG_CUDA(cudaDeviceSynchronize());
+                lv->pmap_d.alloc(n);
+                lv->has_pmap = true;
             }
             lv->mc_tier = lv->n1 <= kMcSmallMaxN1 ? 0 : lv->n1 <= kMcGridMaxN1 ? 1 : 2;
             if (lv->mc_tier == 1) {
@@ -1726,12 +1842,30 @@ int ocmg_hierarchy_create(int n_levels, ocmg_level *const *levels,
         h->tmp.alloc(sizes[n_levels]);
         h->scal.alloc(8);
         setup_subcycle(h.get());
+        setup_collapse(h.get(), kCollapseMaxN);
         *out = h.release();
     });
 }
 
 int ocmg_hierarchy_destroy(ocmg_hierarchy *h) {
     return guarded([&] { delete h; });
+}
+
+int ocmg_hierarchy_collapsed_level(const ocmg_hierarchy *h, int *level_index) {
+    return guarded([&] {
+        OCMG_REQUIRE(h && level_index, "null argument");
+        *level_index = h->col_hi;
+    });
+}
+
+int ocmg_coarse_correction(ocmg_hierarchy *h, int level_index, const double *crhs,
+                           double *corr, void *stream) {
+    return guarded([&] {
+        OCMG_REQUIRE(h && crhs && corr, "null argument");
+        OCMG_REQUIRE(level_index >= 1 && level_index <= (int)h->levels.size(),
+                     "level index out of range");
+        coarse_correction(h, level_index, crhs, corr, as_stream(stream));
+    });
 }
 
 int ocmg_cycle(ocmg_hierarchy *h, double *x, const double *f, void *stream) {
@@ -1883,6 +2017,16 @@ extern "C" int ocmg__debug_hierarchy_fuse(ocmg_hierarchy *h, int on) {
             h->sub_hi = 0;
         h->graph_x = nullptr;  // recapture
         h->graph_f = nullptr;
+    });
+}
+
+// internal: collapse the coarse end of a hierarchy's cycle for levels of at
+// most max_n unknowns (0: off), so tests can compare both cycles
+extern "C" int ocmg__debug_hierarchy_collapse(ocmg_hierarchy *h, int64_t max_n, int *col_hi) {
+    return guarded([&] {
+        OCMG_REQUIRE(h, "null hierarchy");
+        setup_collapse(h, max_n < 0 ? kCollapseMaxN : max_n);
+        if (col_hi) *col_hi = h->col_hi;
     });
 }
 

@@ -227,9 +227,13 @@ __device__ __forceinline__ void gs_cp16(double *dst, const double *src) {
 template <bool FAST>
 __global__ void __launch_bounds__(kGsSmallThreads, 1)
     k_p1_gs_small(int n1, const double *__restrict__ T, int forward,
-                  double *__restrict__ x, double *__restrict__ r) {
+                  double *__restrict__ x, double *__restrict__ r, int64_t bstride) {
     extern __shared__ __align__(16) double gs_sm[];
     const int N = n1 * n1;
+    // independent problems per CTA (the dense-map build sweeps unit
+    // residuals: CTA j works on x + j * bstride, r + j * bstride)
+    x += blockIdx.x * bstride;
+    r += blockIdx.x * bstride;
     double *sr = gs_sm, *sx = gs_sm + 2 * N, *sT = gs_sm + 4 * N;
     // 2N doubles per array: n1 odd => N odd, 2N even, 16-byte chunks
     for (int i = 2 * threadIdx.x; i < 2 * N; i += 2 * blockDim.x) {

@@ -320,8 +320,8 @@ class _RankState:
 class StripMultigrid:
     """The BASELINE V/W cycle with its fine levels split into row strips
     (SURVEY.md §8(e)).  Levels whose strips would be thinner than the 15
-    ghost rows of a sweep are gathered: every rank runs the same single-GPU
-    sub-cycle on them (ocmg_cycle of the hierarchy topped there).
+    ghost rows of a sweep are gathered: every rank applies the same
+    single-GPU coarse correction to them (ocmg_coarse_correction).
 
     Per partitioned level visit: x ghost (1 row) -> residual rows; per sweep
     r ghost (15 rows) -> strip sweep (residual ping-pong); r ghost (1 row) ->
@@ -345,6 +345,11 @@ class StripMultigrid:
         self.mg, self.comm = mg, comm
         n1s = [2 ** s.level + 1 for s in mg.systems]
         first, bounds = nested_bounds(n1s, world_size)
+        # levels the single-GPU cycle has collapsed into a dense coarse
+        # correction are never visited: the partition starts above them
+        col = ctypes.c_int()
+        _lib.call("ocmg_hierarchy_collapsed_level", mg.native().handle, ctypes.byref(col))
+        first = max(first, col.value + 1)
         if first < 2:
             raise ValueError("partitioned levels must leave a gathered "
                              "sub-hierarchy of at least one smoothed level")
@@ -413,11 +418,6 @@ class StripMultigrid:
                 self._sweep(i, False)
 
     def _visit(self, i):
-        if i == self.gather:
-            self.comm.allgather(self.states, i, "f")
-            for st in self.states:
-                self.mg.cycle(i, st.x[i], st.f[i])
-            return
         self._resid(i)
         self._smooth(i, self.nu_pre)
         self.comm.exchange(self.states, i, "r", 1)
@@ -426,10 +426,21 @@ class StripMultigrid:
             cy0, cy1 = st.bounds[i - 1]
             _lib.call("ocmg_restrict_rows", t.handle, _lib.dptr(st.r[i]),
                       _lib.dptr(st.f[i - 1]), cy0, cy1, _lib.stream_ptr())
-            st.x[i - 1].zero_()
-        rec = 2 if (self.w and i - 1 > 0) else 1
-        for _ in range(rec):
-            self._visit(i - 1)
+        if i - 1 == self.gather:
+            # the gathered coarse end: every rank applies the single-GPU
+            # coarse correction (rec sub-cycles, or the collapsed map) to the
+            # whole gathered right-hand side -- the call ocmg_cycle makes
+            self.comm.allgather(self.states, i - 1, "f")
+            h = self.mg.native().handle
+            for st in self.states:
+                _lib.call("ocmg_coarse_correction", h, i, _lib.dptr(st.f[i - 1]),
+                          _lib.dptr(st.x[i - 1]), _lib.stream_ptr())
+        else:
+            for st in self.states:
+                st.x[i - 1].zero_()
+            rec = 2 if (self.w and i - 1 > 0) else 1
+            for _ in range(rec):
+                self._visit(i - 1)
         if i - 1 >= self.first:
             self.comm.exchange(self.states, i - 1, "x", 1)
         for st in self.states:

@@ -30,9 +30,11 @@ case "$job" in
     make -B -C paper_1502_03917_b200/csrc > /dev/null 2>&1 ;;
   solves)     # config-3 solves at coarsest L1 and L3, both modes
     timeout 900 python scripts/solve_c3.py 12 1 3 > gpurun_out/solve_c3.log 2>&1 ;;
-  wcycle)     # launch list of one exact-order W-cycle at coarsest L1
-    timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-      --log-file gpurun_out/wcycle_exact_l1.csv python scripts/wcycle_launches.py 12 w wavefront 1 > gpurun_out/wcycle.log 2>&1 ;;
+  wcycle)     # launch lists of one W-cycle at coarsest L1, both NE-GS modes
+    for m in wavefront multicolour; do
+      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+        --log-file gpurun_out/wcycle_${m}_l1.csv python scripts/wcycle_launches.py 12 w $m 1 > gpurun_out/wcycle_$m.log 2>&1
+    done ;;
   micro)      # micro-benchmarks (built in place)
     for m in micro_lat micro_chain micro_wfchain micro_fp64; do
       nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a --fmad=false -o scripts/$m scripts/$m.cu && ./scripts/$m

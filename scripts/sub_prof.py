@@ -10,9 +10,11 @@ import paper_1502_03917_b200 as P  # noqa: E402
 from paper_1502_03917_b200 import _lib  # noqa: E402
 
 cyc = sys.argv[1] if len(sys.argv) > 1 else "w"
-cfg = P.CycleConfig(smoother=P.SmootherKind("lsgs"), cycle=cyc, coarsest_level=3,
+co = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+top = int(sys.argv[3]) if len(sys.argv) > 3 else 5
+cfg = P.CycleConfig(smoother=P.SmootherKind("lsgs"), cycle=cyc, coarsest_level=co,
                     gs_mode="multicolour")
-mg = P.build_solver("poisson", 5, 1e-6, cfg)
+mg = P.build_solver("poisson", top, 1e-6, cfg)
 h = mg.native().handle
 n = mg.finest.n
 x = torch.zeros(n, dtype=torch.float64, device="cuda")
@@ -38,7 +40,7 @@ def sub_ops(j, w):
     for _ in range(2 if (w and j - 1 > 0) else 1):
         sub_ops(j - 1, w)
     ops.append(("prolong", j)); ops.append(("resid", j)); ops.extend([("sweepF", j)] * 2)
-sub_ops(2, cyc == "w")
+sub_ops(top - co, cyc == "w")
 for (nm, j), dt in zip(ops, d):
     agg[(nm, j)].append(dt)
 for k, v in sorted(agg.items()):

@@ -357,6 +357,7 @@ def test_fused_coarse_block_is_bit_identical(cycle, smoother, k, coarsest):
     f = P.baseline_rhs(mg.finest, 0, add_sine=True)
     fn = _lib.load().ocmg__debug_hierarchy_fuse
     fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    set_collapse(mg, 0)  # the fused block, not the collapsed map
     xs, hs = [], []
     for on in (1, 0):
         _lib.check(fn(mg.native().handle, on))
@@ -365,6 +366,54 @@ def test_fused_coarse_block_is_bit_identical(cycle, smoother, k, coarsest):
         hs.append(hist)
     assert np.array_equal(xs[0], xs[1])
     assert hs[0] == hs[1]
+
+
+def set_collapse(mg, max_n):
+    """Collapse the coarse end of mg's finest hierarchy for levels of at
+    most max_n unknowns (0 off, -1 the library default); returns the
+    collapsed hierarchy index (0: none)."""
+    import ctypes
+    fn = _lib.load().ocmg__debug_hierarchy_collapse
+    fn.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int)]
+    out = ctypes.c_int()
+    _lib.check(fn(mg.native().handle, max_n, ctypes.byref(out)))
+    return out.value
+
+
+@pytest.mark.parametrize("prob,k,cycle,smoother,mode,co", [
+    ("poisson", 8, "w", "lsgs", "wavefront", 1),
+    ("poisson", 8, "w", "lsgs", "multicolour", 1),
+    ("poisson", 7, "v", "slsgs", "wavefront", 2),
+    ("poisson", 7, "w", "normal", "multicolour", 1),
+    ("poisson", 7, "w", "cgs", "multicolour", 3),
+    ("stokes", 4, "w", "lsgs", "wavefront", 1),
+    ("stokes", 4, "v", "normal", "multicolour", 1)])
+def test_collapsed_coarse_end_matches_per_level_cycle(prob, k, cycle, smoother, mode, co):
+    """The coarse end of the cycle as one dense map (setup_collapse: the
+    coarse correction of the deepest levels built column by column from the
+    device's own sub-cycle on unit vectors) gives the per-level cycle's
+    iterates to 1e-12 of max|x| and the same residual history to 1e-9."""
+    kind = (P.SmootherKind("normal", tau=0.35 if prob == "stokes" else 0.4)
+            if smoother == "normal" else P.SmootherKind(smoother))
+    cfg = P.CycleConfig(smoother=kind, cycle=cycle, coarsest_level=co, gs_mode=mode)
+    mg = P.build_solver(prob, k, 1e-4, cfg)
+    f = P.baseline_rhs(mg.finest, 0, add_sine=False)
+    xs, hs, cols = [], [], []
+    for max_n in (0, -1):
+        cols.append(set_collapse(mg, max_n))
+        x, hist = mg.solve_to_tolerance(f, tol=0.0, max_cycles=4)
+        xs.append(host(x))
+        hs.append(np.array(hist))
+    assert cols[0] == 0 and cols[1] >= 1, cols
+    assert np.abs(xs[1] - xs[0]).max() <= 1e-12 * np.abs(xs[0]).max()
+    assert np.allclose(hs[1], hs[0], rtol=1e-9, atol=0)
+
+
+def test_reference_mode_never_collapses():
+    cfg = P.CycleConfig(smoother=P.SmootherKind("lsgs"), cycle="w", coarsest_level=1,
+                        gs_mode="reference")
+    mg = P.build_solver("poisson", 7, 1e-4, cfg)
+    assert set_collapse(mg, -1) == 0
 
 
 @pytest.mark.parametrize("k,ws,cycle,smoother,co", [(8, 2, "v", "lsgs", 3),
