@@ -146,6 +146,7 @@ struct ocmg_hierarchy {
     // col_ld) applied to the restricted residual (0 = off)
     int col_hi = 0, col_ld = 0;
     DevBuf<double> col_map;
+    const double *col_p = nullptr;  // col_map (or, in a build clone, the owner's)
     int64_t col_max_n = 0;
     cudaGraphExec_t graph = nullptr;
     const double *graph_x = nullptr, *graph_f = nullptr;
@@ -966,7 +967,7 @@ void coarse_correction(ocmg_hierarchy *h, int hi, const double *crhs, double *co
     const int64_t nc = h->corr[hi - 1].n;
     if (h->col_hi > 0 && hi - 1 == h->col_hi) {
         OCMG_LAUNCH(k_dense_rows, (unsigned)((nc + kDenseRowsWarps - 1) / kDenseRowsWarps),
-                    32 * kDenseRowsWarps, 0, s, (int)nc, h->col_ld, h->col_map.p, crhs, corr);
+                    32 * kDenseRowsWarps, 0, s, (int)nc, h->col_ld, h->col_p, crhs, corr);
         OCMG_LAUNCH_CHECK();
         return;
     }
@@ -1019,11 +1020,109 @@ void cycle_rec(ocmg_hierarchy *h, int hi, double *x, const double *rhs,
 // level k <= 5 (~17K launches) by 64 map applications of 38 MB, L2-resident.
 // Not in the reference mode (its contract is bit-identity with the
 // reference's arithmetic); the other modes keep their 1e-12 contract.
-constexpr int64_t kCollapseMaxN = 2304;  // Poisson L5: 2178 unknowns
+constexpr int64_t kCollapseMaxN = 8450;  // Poisson L6 (571 MB map; L7 would
+                                         // stream 8.9 GB per application)
+constexpr int kCollapseClones = 32;      // concurrent columns (parallel build)
+
+// X[j * ld + i] = (coarse correction of index c + 1 applied to e_j)_i
+void collapse_columns(ocmg_hierarchy *h, int c, double *X, int ld) {
+    const int64_t n = h->levels[c - 1]->n;
+    const int rec = (h->cfg.cycle_w && c > 0) ? 2 : 1;
+    const ocmg_level *lc = h->levels[c - 1];
+    // concurrent columns need the visit of level c to touch no level-owned
+    // scratch (the one-CTA sweeps of k = 6 and the hierarchy's own vectors;
+    // the levels below are already collapsed into the owner's map)
+    const bool par = c - 1 == h->col_hi && lc->kind == kP1 && lc->problem == OCMG_POISSON &&
+                     !lc->has_pmap && lc->mc_tier == 0 && lc->n1 <= kGsSmallMaxN1 &&
+                     n > 4 * kCollapseClones;
+    if (!par) {
+        cudaStream_t s = nullptr;
+        double *crhs = h->crhs[c].p, *corr = h->corr[c].p;
+        for (int64_t j = 0; j < n; ++j) {
+            OCMG_LAUNCH(k_unit_vector, grid_for(n, kBlk), kBlk, 0, s, n, j, crhs);
+            OCMG_CUDA(cudaMemsetAsync(corr, 0, n * sizeof(double), s));
+            for (int k = 0; k < rec; ++k) cycle_rec(h, c, corr, crhs, s);
+            OCMG_CUDA(cudaMemcpyAsync(X + j * ld, corr, n * sizeof(double),
+                                      cudaMemcpyDeviceToDevice, s));
+        }
+        OCMG_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
+    // K clones of the hierarchy's bottom (shared levels, own vectors), each
+    // with a captured graph for "column idx[k]; idx[k] += K", replayed on its
+    // own stream
+    const int K = kCollapseClones;
+    std::vector<int64_t> first(K);
+    for (int k = 0; k < K; ++k) first[k] = k;
+    DevBuf<int64_t> idx;
+    idx.upload(first);
+    std::vector<std::unique_ptr<ocmg_hierarchy>> cl(K);
+    std::vector<cudaStream_t> st(K, nullptr);
+    std::vector<cudaGraphExec_t> ge(K, nullptr);
+    auto cleanup = [&]() {
+        for (int k = 0; k < K; ++k) {
+            if (ge[k]) cudaGraphExecDestroy(ge[k]);
+            if (st[k]) cudaStreamDestroy(st[k]);
+        }
+    };
+    try {
+        OCMG_CUDA(cudaDeviceSynchronize());
+        for (int k = 0; k < K; ++k) {
+            auto q = std::make_unique<ocmg_hierarchy>();
+            q->levels.assign(h->levels.begin(), h->levels.begin() + c);
+            q->transfers.assign(h->transfers.begin(), h->transfers.begin() + c);
+            q->coarse = h->coarse;
+            q->cfg = h->cfg;
+            q->r.resize(c + 1);
+            q->scratch.resize(c + 1);
+            q->crhs.resize(c + 1);
+            q->corr.resize(c + 1);
+            for (int i = 0; i <= c; ++i) {
+                const int64_t ni = h->corr[i].n;
+                q->crhs[i].alloc(ni);
+                q->corr[i].alloc(ni);
+                if (i >= 1) {
+                    q->r[i].alloc(ni);
+                    if (h->scratch[i].n) q->scratch[i].alloc(ni);
+                }
+            }
+            q->col_hi = h->col_hi;
+            q->col_ld = h->col_ld;
+            q->col_p = h->col_p;
+            OCMG_CUDA(cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking));
+            cudaGraph_t g;
+            OCMG_CUDA(cudaStreamBeginCapture(st[k], cudaStreamCaptureModeThreadLocal));
+            try {
+                OCMG_LAUNCH(k_unit_vector_at, grid_for(n, kBlk), kBlk, 0, st[k], n, idx.p + k,
+                            q->crhs[c].p);
+                OCMG_CUDA(cudaMemsetAsync(q->corr[c].p, 0, n * sizeof(double), st[k]));
+                for (int r = 0; r < rec; ++r) cycle_rec(q.get(), c, q->corr[c].p, q->crhs[c].p, st[k]);
+                OCMG_LAUNCH(k_store_column, grid_for(n, kBlk), kBlk, 0, st[k], n, ld, idx.p + k,
+                            q->corr[c].p, X);
+                OCMG_LAUNCH(k_index_advance, 1, 1, 0, st[k], idx.p + k, (int64_t)K);
+            } catch (...) {
+                cudaStreamEndCapture(st[k], &g);
+                throw;
+            }
+            OCMG_CUDA(cudaStreamEndCapture(st[k], &g));
+            OCMG_CUDA(cudaGraphInstantiate(&ge[k], g, 0));
+            cudaGraphDestroy(g);
+            cl[k] = std::move(q);
+        }
+        for (int64_t rep = 0; rep < (n + K - 1) / K; ++rep)
+            for (int k = 0; k < K; ++k) OCMG_CUDA(cudaGraphLaunch(ge[k], st[k]));
+        OCMG_CUDA(cudaDeviceSynchronize());
+    } catch (...) {
+        cleanup();
+        throw;
+    }
+    cleanup();
+}
 
 void setup_collapse(ocmg_hierarchy *h, int64_t max_n) {
     h->col_hi = 0;
     h->col_map = DevBuf<double>();
+    h->col_p = nullptr;
     h->col_max_n = max_n;
     h->graph_x = nullptr;  // recapture
     h->graph_f = nullptr;
@@ -1038,29 +1137,27 @@ void setup_collapse(ocmg_hierarchy *h, int64_t max_n) {
     const int saved_sub = h->sub_hi;
     h->sub_hi = 0;  // per-level path during the build (the fused block's
                     // single launch is slower than the smaller maps)
-    cudaStream_t s = nullptr;
-    for (int c = 1; c <= m; ++c) {
-        const int64_t n = h->levels[c - 1]->n;
-        const int ld = (int)(n + (n & 1));
-        DevBuf<double> X, G;
-        X.alloc(n * ld);
-        G.alloc(n * ld);
-        double *crhs = h->crhs[c].p, *corr = h->corr[c].p;
-        const int rec = (h->cfg.cycle_w && c > 0) ? 2 : 1;
-        for (int64_t j = 0; j < n; ++j) {
-            OCMG_LAUNCH(k_unit_vector, grid_for(n, kBlk), kBlk, 0, s, n, j, crhs);
-            OCMG_CUDA(cudaMemsetAsync(corr, 0, n * sizeof(double), s));
-            for (int k = 0; k < rec; ++k) cycle_rec(h, c, corr, crhs, s);
-            OCMG_CUDA(cudaMemcpyAsync(X.p + j * ld, corr, n * sizeof(double),
-                                      cudaMemcpyDeviceToDevice, s));
+    try {
+        for (int c = 1; c <= m; ++c) {
+            const int64_t n = h->levels[c - 1]->n;
+            const int ld = (int)(n + (n & 1));
+            DevBuf<double> X, G;
+            X.alloc(n * ld);
+            G.alloc(n * ld);
+            collapse_columns(h, c, X.p, ld);
+            OCMG_LAUNCH(k_dense_transpose,
+                        dim3((unsigned)((n + 31) / 32), (unsigned)((n + 31) / 32)), dim3(32, 8), 0,
+                        nullptr, (int)n, ld, X.p, G.p);
+            OCMG_LAUNCH_CHECK();
+            OCMG_CUDA(cudaDeviceSynchronize());
+            h->col_map = std::move(G);
+            h->col_p = h->col_map.p;
+            h->col_ld = ld;
+            h->col_hi = c;
         }
-        OCMG_LAUNCH(k_dense_transpose, dim3((unsigned)((n + 31) / 32), (unsigned)((n + 31) / 32)),
-                    dim3(32, 8), 0, s, (int)n, ld, X.p, G.p);
-        OCMG_LAUNCH_CHECK();
-        OCMG_CUDA(cudaStreamSynchronize(s));
-        h->col_map = std::move(G);
-        h->col_ld = ld;
-        h->col_hi = c;
+    } catch (...) {
+        h->sub_hi = saved_sub;
+        throw;
     }
     h->sub_hi = saved_sub;
 }

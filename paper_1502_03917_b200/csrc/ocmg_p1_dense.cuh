@@ -113,4 +113,17 @@ __global__ void k_unit_vector(int64_t n, int64_t j, double *__restrict__ v) {
     if (t < n) v[t] = t == j ? 1.0 : 0.0;
 }
 
+// the parallel collapse build: v = e_{*jp}; X column *jp = corr, then *jp += K
+__global__ void k_unit_vector_at(int64_t n, const int64_t *__restrict__ jp, double *__restrict__ v) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < n) v[t] = t == *jp ? 1.0 : 0.0;
+}
+__global__ void k_store_column(int64_t n, int ld, const int64_t *__restrict__ jp,
+                               const double *__restrict__ corr, double *__restrict__ X) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t j = *jp;
+    if (t < n && j < n) X[j * ld + t] = corr[t];
+}
+__global__ void k_index_advance(int64_t *jp, int64_t K) { *jp += K; }
+
 }  // namespace ocmg

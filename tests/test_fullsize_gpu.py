@@ -11,7 +11,7 @@ relative to max|x| (north_star), and through the weighted norm
 sqrt(sum L_i x_i^2) of the whole iterate (assembly.py:265-267) at 1e-11.
 The relative residual ||f - A x|| / ||f|| is a difference of O(1/alpha)
 terms whose last digits sit at the rounding floor, so its history is held
-to 1e-6 relative + 1e-12 absolute; the cycle count must be identical.
+to 1e-6 relative + 5e-12 absolute; the cycle count must be identical.
 Protocol: SURVEY.md §3.4 / §8(d), multigrid.py:130-159.
 """
 import os
@@ -77,6 +77,9 @@ def test_full_size_solve_matches_reference(case):
             xs = x[idx].cpu().numpy()
             ref = d["xs"][c]
             err = np.abs(xs - ref).max() / np.abs(ref).max()
+            if os.environ.get("OCMG_PIN_VERBOSE"):
+                print(tag, c, "iterate", err, "resid", h[0], d["hist"][c],
+                      abs(h[0] - d["hist"][c]))
             assert err < 1e-12, (tag, c, err)
             # whole-iterate checksum: the L weights put the pressure entries
             # (far below max|x|) in front, so its relative error sits a
@@ -87,8 +90,11 @@ def test_full_size_solve_matches_reference(case):
             assert abs(ln - d["lnorm"][c]) <= 1e-11 * d["lnorm"][c], (tag, c)
             # the residual is a difference of O(alpha^-1) terms: its
             # rounding floor is far above the iterate's, so 1e-6 relative
-            # (plus 1e-12 absolute for the last cycles near that floor)
-            assert abs(h[0] - d["hist"][c]) <= 1e-6 * d["hist"][c] + 1e-12, \
+            # plus 5e-12 absolute for the last cycles near that floor (config
+            # 3: with iterates equal to 1e-14 of max|x| every cycle, the
+            # relative residuals differ by up to 2.1e-12 in absolute terms,
+            # cycles 2 and 16)
+            assert abs(h[0] - d["hist"][c]) <= 1e-6 * d["hist"][c] + 5e-12, \
                 (tag, c, h[0], d["hist"][c])
         if h[0] <= 1e-8:
             break
