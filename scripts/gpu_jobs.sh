@@ -28,6 +28,17 @@ case "$job" in
     (cd paper_1502_03917_b200/csrc && make -B NVFLAGS="$NVBASE -DOCMG_WF_PROFILE" > /dev/null 2>&1)
     timeout 120 python scripts/wf_prof.py 12 > gpurun_out/wf_prof12.log 2>&1
     make -B -C paper_1502_03917_b200/csrc > /dev/null 2>&1 ;;
+  wfprofab)   # per-warp stage timers of WF_VARIANTS (profile build + extra flags)
+    IFS=';' read -ra vs <<< "${WF_VARIANTS:-}"
+    i=0
+    for v in "${vs[@]}"; do
+      (cd paper_1502_03917_b200/csrc && make -B NVFLAGS="$NVBASE -DOCMG_WF_PROFILE $v" > /dev/null 2>&1)
+      echo "== variant [$v]" > gpurun_out/wfprof_v$i.log
+      timeout 120 python scripts/wf_prof.py 12 >> gpurun_out/wfprof_v$i.log 2>&1
+      cp gpurun_out/wfprof_k12.npy gpurun_out/wfprof_v$i.npy
+      i=$((i+1))
+    done
+    make -B -C paper_1502_03917_b200/csrc > /dev/null 2>&1 ;;
   solves)     # config-3 solves at coarsest L1 and L3, both modes
     timeout 900 python scripts/solve_c3.py 12 1 3 > gpurun_out/solve_c3.log 2>&1 ;;
   wcycle)     # launch lists of one W-cycle at coarsest L1, both NE-GS modes
@@ -35,9 +46,17 @@ case "$job" in
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file gpurun_out/wcycle_${m}_l1.csv python scripts/wcycle_launches.py 12 w $m 1 > gpurun_out/wcycle_$m.log 2>&1
     done ;;
+  wfab)       # exact-order sweep A/B: WF_VARIANTS="flags1;flags2;..." (extra nvcc -D flags)
+    IFS=';' read -ra vs <<< "${WF_VARIANTS:-}"
+    for v in "${vs[@]}"; do
+      (cd paper_1502_03917_b200/csrc && make -B NVFLAGS="$NVBASE $v" > /dev/null 2>&1)
+      echo "== variant [$v]"
+      timeout 200 python scripts/wf_time.py ${WF_LEVELS:-10 12} 2>&1 | grep sweep
+    done > gpurun_out/wfab.log 2>&1
+    make -B -C paper_1502_03917_b200/csrc > /dev/null 2>&1 ;;
   micro)      # micro-benchmarks (built in place)
     for m in micro_lat micro_chain micro_wfchain micro_fp64; do
       nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a --fmad=false -o scripts/$m scripts/$m.cu && ./scripts/$m
     done > gpurun_out/micro.log 2>&1 ;;
-  *) echo "usage: bash scripts/gpu_jobs.sh {tests|fullsize|evidence|wavefront|solves|wcycle|micro}" ;;
+  *) echo "usage: bash scripts/gpu_jobs.sh {tests|fullsize|evidence|wavefront|solves|wcycle|wfab|micro}" ;;
 esac
