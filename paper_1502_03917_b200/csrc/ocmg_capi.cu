@@ -15,6 +15,7 @@
 #include "ocmg_p1.cuh"
 #include "ocmg_p1_tiled.cuh"
 #include "ocmg_p1_mc.cuh"
+#include "ocmg_p1_mc2.cuh"
 #include "ocmg_p1_mc_small.cuh"
 #include "ocmg_p1_gsdiag.cuh"
 #include "ocmg_p1_dense.cuh"
@@ -536,7 +537,7 @@ bool p1_mc_sweep(const ocmg_level *lv, bool forward, double *x, double *r,
     P.rin = r;
     P.rout = rout;
     P.x = x;
-    mcs_launch(P, lv->mc.grid, s);
+    mc_launch(P, lv->mc.grid, s);
     OCMG_LAUNCH_CHECK();
     return true;
 }
@@ -1426,10 +1427,11 @@ int ocmg_level_create_p1(int k, double alpha, const double *tables,
         {
             // per call: the attribute is per device, and cheap to set
             mcs_set_smem();
+            mc2_set_smem();
             int dev = 0, sms = 148;
             OCMG_CUDA(cudaGetDevice(&dev));
             OCMG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-            lv->mc = mcs_plan(lv->n1, sms);
+            lv->mc = mc_plan(lv->n1, sms);
             // per call: the attribute is per device, and cheap to set
             OCMG_CUDA(cudaFuncSetAttribute(k_p1_mc_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            mc_small_smem(kMcSmallMaxN1)));
@@ -1668,7 +1670,7 @@ int ocmg_ne_gs_sweep_strip(const ocmg_level *lv, int forward, int y_begin,
         int dev = 0, sms = 148;
         OCMG_CUDA(cudaGetDevice(&dev));
         OCMG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        const McsPlan pl = mcs_plan(n1, sms, y_end - y_begin);
+        const McsPlan pl = mc_plan(n1, sms, y_end - y_begin);
         McsParams P{};
         P.n1 = n1;
         P.nstrips = pl.nstrips;
@@ -1683,7 +1685,7 @@ int ocmg_ne_gs_sweep_strip(const ocmg_level *lv, int forward, int y_begin,
         P.rin = r_in - (int64_t)slab_begin * n1;
         P.rout = r_out - (int64_t)slab_begin * n1;
         P.x = x - (int64_t)slab_begin * n1;
-        mcs_launch(P, pl.grid, as_stream(stream));
+        mc_launch(P, pl.grid, as_stream(stream));
         OCMG_LAUNCH_CHECK();
         if (ops) *ops = 2 * lv->nnz * (int64_t)(y_end - y_begin) / n1;
     });
@@ -2102,6 +2104,14 @@ extern "C" int ocmg__debug_mc_passes(const ocmg_level *lv, int forward, double *
         OCMG_LAUNCH_CHECK();
     });
 }
+
+#ifdef MC2_PROF
+extern "C" int ocmg__debug_mc2_prof(unsigned long long *out, int n) {
+    return guarded([&] {
+        OCMG_CUDA(cudaMemcpyFromSymbol(out, mc2_prof, sizeof(unsigned long long) * n));
+    });
+}
+#endif
 
 // internal: switch the fused coarse block of a hierarchy off (0) or back on
 // (1), so tests can compare the fused and per-level cycles

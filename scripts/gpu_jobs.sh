@@ -54,9 +54,20 @@ case "$job" in
       timeout 200 python scripts/wf_time.py ${WF_LEVELS:-10 12} 2>&1 | grep sweep
     done > gpurun_out/wfab.log 2>&1
     make -B -C paper_1502_03917_b200/csrc > /dev/null 2>&1 ;;
+  mc2)        # the experimental rolling-window multicolour kernel: parity, timing against
+              # the default kernel, per-warp cycle counters (-DMC2_PROF build)
+    for k in 7 8 10 12; do OCMG_MC_SWEEP=roll timeout 300 python scripts/mc_check.py $k; done > gpurun_out/mc2_check.log 2>&1
+    { OCMG_MC_SWEEP=roll timeout 200 python scripts/kbench.py --ops multicolour | tail -1
+      timeout 200 python scripts/kbench.py --ops multicolour | tail -1; } > gpurun_out/mc2_kbench.log 2>&1
+    (cd paper_1502_03917_b200/csrc && make -B NVFLAGS="$NVBASE -DMC2_PROF" > /dev/null 2>&1)
+    OCMG_MC_SWEEP=roll timeout 200 python scripts/mc2_prof.py 12 > gpurun_out/mc2_prof.log 2>&1
+    make -B -C paper_1502_03917_b200/csrc > /dev/null 2>&1
+    for m in micro_node micro_dfma_lat; do
+      nvcc -O3 -std=c++17 --fmad=false -gencode arch=compute_100a,code=sm_100a -o /tmp/$m scripts/$m.cu && /tmp/$m
+    done > gpurun_out/mc2_micro.log 2>&1 ;;
   micro)      # micro-benchmarks (built in place)
     for m in micro_lat micro_chain micro_wfchain micro_fp64; do
       nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a --fmad=false -o scripts/$m scripts/$m.cu && ./scripts/$m
     done > gpurun_out/micro.log 2>&1 ;;
-  *) echo "usage: bash scripts/gpu_jobs.sh {tests|fullsize|evidence|wavefront|solves|wcycle|wfab|micro}" ;;
+  *) echo "usage: bash scripts/gpu_jobs.sh {tests|fullsize|evidence|wavefront|solves|wcycle|wfab|mc2|micro}" ;;
 esac

@@ -295,6 +295,29 @@ def test_multicolour_one_launch_matches_colour_passes(k, forward):
     assert torch.equal(r, r2)
 
 
+def test_rolling_window_multicolour_kernel_is_bit_identical():
+    """The experimental rolling-window one-launch kernel (ocmg_p1_mc2.cuh,
+    opt-in with OCMG_MC_SWEEP=roll, read once per process) against the
+    colour passes and, through the strip entry point, against itself on the
+    whole level: child processes, since the switch is per process."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, OCMG_MC_SWEEP="roll")
+    for k in (7, 10):
+        out = subprocess.run([sys.executable, os.path.join(root, "scripts", "mc_check.py"), str(k)],
+                             env=env, capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        lines = [ln for ln in out.stdout.splitlines() if ln.startswith("k=")]
+        assert len(lines) == 2 and all("equal=True" in ln for ln in lines), out.stdout
+    out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                          os.path.join(root, "tests", "test_gpu_parity.py"), "-k",
+                          "test_strip_sweeps_match_single_gpu and 10"],
+                         env=env, capture_output=True, text=True, timeout=900, cwd=root)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+
+
 @pytest.mark.parametrize("k", [4, 8, 10])
 @pytest.mark.parametrize("mode", ["multicolour", "wavefront"])
 def test_sweep_into_matches_in_place(k, mode):
