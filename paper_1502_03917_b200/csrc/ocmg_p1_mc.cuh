@@ -83,7 +83,18 @@ constexpr int RING = K * D + K + LAG + 1;
 constexpr int WPC = MCS_WPC;
 constexpr int KW = K / WPC;          // rows per colour warp and superstep
 static_assert(K % WPC == 0, "rows per superstep split evenly over a colour's warps");
-constexpr int NT = 32 * (NC * WPC + 1);  // colour warps + the boundary-column warp
+#ifndef MCS_ND
+#define MCS_ND 4
+#endif
+// duty warps: they load the rows (cp.async) and write the final ones back
+// while the colour warps compute.  With MCS_ND = 0 every thread shares the
+// duties before its vertex updates, as in round 1: ncu's source page put 37%
+// of a colour warp's time into that part (200 instructions of predicates,
+// selects and 64-bit pointer arithmetic in front of the 200 of the update).
+constexpr int ND = MCS_ND;
+constexpr int NCW = NC * WPC + 1;        // colour warps + the boundary-column warp
+constexpr int NT = 32 * (NCW + ND);
+constexpr int NDT = ND ? 32 * ND : NT;   // threads that share the duties
 constexpr int W = MCS_W;           // owned columns per CTA (at most)
 constexpr int STRIDE = W + 2 * H + 2;  // r ring row: columns xl-1 .. xr
 constexpr int RS = STRIDE * 16;    // r ring row bytes: (state, adjoint) pairs
@@ -95,8 +106,8 @@ constexpr int CROW = 30;           // class row: W (14), A (14), 1/n_diag, pad
 constexpr int X_OFF = RING * RS;
 constexpr int CLS_OFF = X_OFF + RING * XS;
 constexpr int SMEM = CLS_OFF + 7 * 2 * CROW * 8;
-constexpr int NLD = (2 * STRIDE + 2 * W + NT - 1) / NT;  // row-load entries per thread
-constexpr int NST = (2 * W + NT - 1) / NT;               // row-store pairs per thread
+constexpr int NLD = (2 * STRIDE + 2 * W + NDT - 1) / NDT;  // row-load entries per duty thread
+constexpr int NST = (2 * W + NDT - 1) / NDT;               // row-store pairs per duty thread
 static_assert((W + 2 * H + 6) / 7 <= 31, "one warp per colour-row, lane 31 free");
 static_assert(SMEM + 1024 <= 228 * 1024, "one CTA per SM");
 
@@ -233,13 +244,15 @@ __global__ void __launch_bounds__(mcs::NT, 1) k_p1_mc_sweep(const __grid_constan
     // outside [xl, xr) and for rows past rmax; [2 STRIDE, 2 STRIDE + 2 W): x
     // (field, owned column), rows Y0 .. Y1-1 only.
     const int rmax = min(Yhi, n1 - 1);
+    const bool duty = ND == 0 || q >= NCW;          // this thread shares the duties
+    const int dt = ND ? tid - 32 * NCW : tid;       // its index among the duty threads
     bool lisx[NLD], lact[NLD], lhas[NLD];
     unsigned loff[NLD];
     const double *lp[NLD];  // entry's element in row Ylo-1 (a valid address if inactive)
 #pragma unroll
     for (int e = 0; e < NLD; ++e) {
-        const int t = tid + e * NT;
-        lhas[e] = t < 2 * STRIDE + 2 * W;
+        const int t = dt + e * NDT;
+        lhas[e] = duty && t < 2 * STRIDE + 2 * W;
         lisx[e] = t >= 2 * STRIDE;
         if (!lisx[e]) {
             const int f = t >= STRIDE, lc = t - f * STRIDE, gx = xl - 1 + lc;
@@ -270,12 +283,14 @@ __global__ void __launch_bounds__(mcs::NT, 1) k_p1_mc_sweep(const __grid_constan
     };
     // prologue: rows Ylo-1 .. Ylo+K (superstep 0), then K rows per superstep
     // 1 .. D-1, one commit group per superstep
-    for (int j = 0; j < K + 2; ++j) load_row();
-    mcs_commit();
-    for (int g = 1; g < D; ++g) {
-#pragma unroll
-        for (int i = 0; i < K; ++i) load_row();
+    if (duty) {
+        for (int j = 0; j < K + 2; ++j) load_row();
         mcs_commit();
+        for (int g = 1; g < D; ++g) {
+#pragma unroll
+            for (int i = 0; i < K; ++i) load_row();
+            mcs_commit();
+        }
     }
 
     // ---- store role: thread -> NST entries t of each leaving row: t < W an
@@ -286,10 +301,10 @@ __global__ void __launch_bounds__(mcs::NT, 1) k_p1_mc_sweep(const __grid_constan
     unsigned soff[NST], srs[NST];
 #pragma unroll
     for (int e = 0; e < NST; ++e) {
-        const int t = tid + e * NT;
+        const int t = dt + e * NDT;
         const bool isx = t >= W;
         const int c = isx ? t - W : t;
-        sact[e] = t < 2 * W && X0 + c < X1;
+        sact[e] = duty && t < 2 * W && X0 + c < X1;
         sp[e] = (isx ? P.x : P.rout) + (int64_t)(Ylo - LAG) * n1 + X0 + c;
         sfs[e] = isx ? P.fs_x : P.fs_out;
         soff[e] = isx ? sm + X_OFF + (unsigned)c * 16u : sm + (unsigned)(X0 - xl + 1 + c) * 16u;
@@ -297,6 +312,43 @@ __global__ void __launch_bounds__(mcs::NT, 1) k_p1_mc_sweep(const __grid_constan
     }
     int srow = Ylo - LAG;                          // next row to leave
     int sslot = (RING - (LAG - 1) % RING) % RING;  // its slot
+
+    const int S_end = (Y1 - Ylo + LAG + K - 1) / K;
+    auto duties = [&]() {
+        // 1. the rows superstep S + D needs first
+#pragma unroll
+        for (int i = 0; i < K; ++i) load_row();
+        mcs_commit();
+        // 2. final rows leave (r pairs, x pairs)
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            if (srow >= Y0 && srow < Y1) {  // CTA-uniform
+#pragma unroll
+                for (int e = 0; e < NST; ++e)
+                    if (sact[e]) {
+                        const double2 v = mcs_lds2(soff[e] + (unsigned)sslot * srs[e]);
+                        sp[e][0] = v.x;
+                        sp[e][sfs[e]] = v.y;
+                    }
+            }
+#pragma unroll
+            for (int e = 0; e < NST; ++e) sp[e] += n1;
+            ++srow;
+            sslot = wrap(sslot + 1);
+        }
+    };
+    if (ND != 0 && q >= NCW) {
+        // ---- the duty warps' loop: the same barriers as the compute warps'
+        mcs_wait<D - 1>();
+        __syncthreads();
+        for (int S = 0; S < S_end; ++S) {
+            duties();
+            mcs_wait<D - 1>();
+            __syncthreads();
+        }
+        mcs_wait<0>();
+        return;
+    }
 
     // ---- compute roles.  Colour warp q = position q of the sweep (colour q
     // forward, 6 - q backward); at superstep S it updates rows
@@ -325,32 +377,11 @@ __global__ void __launch_bounds__(mcs::NT, 1) k_p1_mc_sweep(const __grid_constan
 #pragma unroll
     for (int i = 0; i < NU; ++i) cu[i] = P.cu[i];
     const unsigned cls_s = sm + CLS_OFF;
-    const int S_end = (Y1 - Ylo + LAG + K - 1) / K;
     mcs_wait<D - 1>();
     __syncthreads();
 
     for (int S = 0; S < S_end; ++S) {
-        // 1. the rows superstep S + D needs first
-#pragma unroll
-        for (int i = 0; i < K; ++i) load_row();
-        mcs_commit();
-        // 2. final rows leave (r pairs, x pairs)
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-            if (srow >= Y0 && srow < Y1) {  // CTA-uniform
-#pragma unroll
-                for (int e = 0; e < NST; ++e)
-                    if (sact[e]) {
-                        const double2 v = mcs_lds2(soff[e] + (unsigned)sslot * srs[e]);
-                        sp[e][0] = v.x;
-                        sp[e][sfs[e]] = v.y;
-                    }
-            }
-#pragma unroll
-            for (int e = 0; e < NST; ++e) sp[e] += n1;
-            ++srow;
-            sslot = wrap(sslot + 1);
-        }
+        if (ND == 0) duties();  // 1. rows for superstep S + D in, 2. final rows out
         // 3. vertex updates (independent: same colour, distance >= 3)
         auto rrow = [&](int j) {  // r ring row j (slot sl + j) as double2*
             return reinterpret_cast<double2 *>(smc + wrap(sl + j) * RS);
