@@ -264,7 +264,7 @@ int ocmg_cycle(ocmg_hierarchy *h, double *x, const double *f, void *stream);
  * cycles of index level_index - 1 from zero (rec = 2 for a W-cycle above
  * the coarse solve, multigrid.py:150-152).  Outside the reference mode the
  * library collapses that map for the coarse end of the hierarchy (levels of
- * at most 2304 unknowns below the finest) into one dense matrix built at
+ * at most 8450 unknowns below the finest) into one dense matrix built at
  * ocmg_hierarchy_create from the same device cycle on unit vectors; this
  * call applies whichever form the cycle uses (partitioned cycles call it to
  * stay bit-identical to ocmg_cycle). */

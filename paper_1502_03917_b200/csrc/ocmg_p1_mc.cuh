@@ -433,6 +433,12 @@ __global__ void __launch_bounds__(mcs::NT, 1) k_p1_mc_sweep(const __grid_constan
                 double2 v[KW][7];
 #pragma unroll
                 for (int ii = 0; ii < KW; ++ii) load_v(i0 + ii, xi[ii], v[ii]);
+                // x of the vertices, loaded with their neighbourhoods so that
+                // the x update at the end is an add and a store (a halo
+                // vertex reads some other entry of the rings and drops it)
+                double2 xo[KW];
+#pragma unroll
+                for (int ii = 0; ii < KW; ++ii) xo[ii] = *xent(i0 + ii, xi[ii]);
                 double pa[KW], pb[KW];  // first / second unknown in sweep order
 #pragma unroll
                 for (int ii = 0; ii < KW; ++ii) pa[ii] = node_update_u<FWD ? 0 : 1>(v[ii], cu);
@@ -442,7 +448,10 @@ __global__ void __launch_bounds__(mcs::NT, 1) k_p1_mc_sweep(const __grid_constan
                 for (int ii = 0; ii < KW; ++ii)
                     if (act[ii]) {
                         store_v(i0 + ii, xi[ii], v[ii]);
-                        if (owned(i0 + ii, xi[ii])) x_update(i0 + ii, xi[ii], pa[ii], pb[ii]);
+                        if (owned(i0 + ii, xi[ii]))
+                            *xent(i0 + ii, xi[ii]) =
+                                make_double2(__dadd_rn(xo[ii].x, FWD ? pa[ii] : pb[ii]),
+                                             __dadd_rn(xo[ii].y, FWD ? pb[ii] : pa[ii]));
                     }
             } else {  // a boundary row: per-lane class rows from the global table
 #pragma unroll
