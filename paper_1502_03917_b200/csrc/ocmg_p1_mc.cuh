@@ -201,6 +201,9 @@ __device__ __forceinline__ double2 mcs_lds2(unsigned a) {
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
     return v;
 }
+__device__ __forceinline__ void mcs_sts2(unsigned a, double2 v) {
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
 // node_update with the coefficient row in shared memory (cs: its address,
 // 16-byte aligned; asm volatile keeps the 15 loads next to their use)
 __device__ __forceinline__ double node_update_s(double2 (&v)[7], unsigned cs) {
@@ -377,11 +380,62 @@ __global__ void __launch_bounds__(mcs::NT, 1) k_p1_mc_sweep(const __grid_constan
 #pragma unroll
     for (int i = 0; i < NU; ++i) cu[i] = P.cu[i];
     const unsigned cls_s = sm + CLS_OFF;
+    // The common superstep of a colour warp -- both rows interior and inside
+    // the colour's valid rows -- runs on loop-carried state: the ring
+    // addresses of rows y-1 .. y+2 and of the x rows, the two column offsets
+    // (mod 7 by compare), and the lane's column windows relative to xbase
+    // (its computed columns, its owned columns).  The general path below
+    // recomputes all of it from y, o and sl each superstep (75 dependent
+    // integer instructions in front of the first load, ~340 cycles).
+    constexpr bool kFast = K == 2 && WPC == 1;
+    const int fyA = max(cyl, 3), fyW = max(min(cyh, n1 - 3) - 1 - fyA, 0);  // y_0 range of a fast superstep
+    const int fxlo = max(cxl, 3) - xbase, fxw = max(min(cxr, n1 - 3) - max(cxl, 3), 0);
+    const int oxlo = X0 - xbase, oxw = X1 - X0;
+    const unsigned cb = (unsigned)(xbase - xl + 1) * 16u, xb16 = (unsigned)(xbase - X0) * 16u;
+    const unsigned r_end = sm + RING * RS, x_end = sm + X_OFF + RING * XS;
+    auto nxt_r = [&](unsigned a) { return a + RS == r_end ? sm : a + RS; };
+    auto nxt_x = [&](unsigned a) { return a + XS == x_end ? sm + X_OFF : a + XS; };
+    unsigned ra0 = sm + (unsigned)sl * RS, ra1 = nxt_r(ra0), ra2 = nxt_r(ra1), ra3 = nxt_r(ra2);
+    unsigned xa0 = sm + X_OFF + (unsigned)wrap(sl + 1) * XS, xa1 = nxt_x(xa0);
     mcs_wait<D - 1>();
     __syncthreads();
 
     for (int S = 0; S < S_end; ++S) {
         if (ND == 0) duties();  // 1. rows for superstep S + D in, 2. final rows out
+        if (kFast && !bw && (unsigned)(y - fyA) < (unsigned)fyW) {
+            int o1 = o + 5;
+            o1 -= o1 >= 7 ? 7 : 0;
+            const unsigned c0 = cb + (unsigned)o * 16u, c1 = cb + (unsigned)o1 * 16u;
+            double2 v0[7], v1[7];
+            v0[0] = mcs_lds2(ra0 + c0 - 16); v0[1] = mcs_lds2(ra0 + c0);
+            v0[2] = mcs_lds2(ra1 + c0 - 16); v0[3] = mcs_lds2(ra1 + c0); v0[4] = mcs_lds2(ra1 + c0 + 16);
+            v0[5] = mcs_lds2(ra2 + c0); v0[6] = mcs_lds2(ra2 + c0 + 16);
+            v1[0] = mcs_lds2(ra1 + c1 - 16); v1[1] = mcs_lds2(ra1 + c1);
+            v1[2] = mcs_lds2(ra2 + c1 - 16); v1[3] = mcs_lds2(ra2 + c1); v1[4] = mcs_lds2(ra2 + c1 + 16);
+            v1[5] = mcs_lds2(ra3 + c1); v1[6] = mcs_lds2(ra3 + c1 + 16);
+            const unsigned xe0 = xa0 + xb16 + (unsigned)o * 16u, xe1 = xa1 + xb16 + (unsigned)o1 * 16u;
+            const double2 xo0 = mcs_lds2(xe0), xo1 = mcs_lds2(xe1);
+            const double pa0 = node_update_u<FWD ? 0 : 1>(v0, cu);
+            const double pa1 = node_update_u<FWD ? 0 : 1>(v1, cu);
+            const double pb0 = node_update_u<FWD ? 1 : 0>(v0, cu);
+            const double pb1 = node_update_u<FWD ? 1 : 0>(v1, cu);
+            if ((unsigned)(o - fxlo) < (unsigned)fxw) {
+                mcs_sts2(ra0 + c0 - 16, v0[0]); mcs_sts2(ra0 + c0, v0[1]);
+                mcs_sts2(ra1 + c0 - 16, v0[2]); mcs_sts2(ra1 + c0, v0[3]); mcs_sts2(ra1 + c0 + 16, v0[4]);
+                mcs_sts2(ra2 + c0, v0[5]); mcs_sts2(ra2 + c0 + 16, v0[6]);
+                if ((unsigned)(y - Y0) < (unsigned)(Y1 - Y0) && (unsigned)(o - oxlo) < (unsigned)oxw)
+                    mcs_sts2(xe0, make_double2(__dadd_rn(xo0.x, FWD ? pa0 : pb0),
+                                               __dadd_rn(xo0.y, FWD ? pb0 : pa0)));
+            }
+            if ((unsigned)(o1 - fxlo) < (unsigned)fxw) {
+                mcs_sts2(ra1 + c1 - 16, v1[0]); mcs_sts2(ra1 + c1, v1[1]);
+                mcs_sts2(ra2 + c1 - 16, v1[2]); mcs_sts2(ra2 + c1, v1[3]); mcs_sts2(ra2 + c1 + 16, v1[4]);
+                mcs_sts2(ra3 + c1, v1[5]); mcs_sts2(ra3 + c1 + 16, v1[6]);
+                if ((unsigned)(y + 1 - Y0) < (unsigned)(Y1 - Y0) && (unsigned)(o1 - oxlo) < (unsigned)oxw)
+                    mcs_sts2(xe1, make_double2(__dadd_rn(xo1.x, FWD ? pa1 : pb1),
+                                               __dadd_rn(xo1.y, FWD ? pb1 : pa1)));
+            }
+        } else {
         // 3. vertex updates (independent: same colour, distance >= 3)
         auto rrow = [&](int j) {  // r ring row j (slot sl + j) as double2*
             return reinterpret_cast<double2 *>(smc + wrap(sl + j) * RS);
@@ -496,10 +550,19 @@ __global__ void __launch_bounds__(mcs::NT, 1) k_p1_mc_sweep(const __grid_constan
                 if (owned(bi, xb)) x_update(bi, xb, pa, pb);
             }
         }
+        }
         // advance K rows
         y += K;
         sl = wrap(sl + K);
         o = (o - 2 * K + 7 * K) % 7;
+        if (kFast) {
+            ra0 = ra2;
+            ra1 = ra3;
+            ra2 = nxt_r(ra3);
+            ra3 = nxt_r(ra2);
+            xa0 = nxt_x(xa1);
+            xa1 = nxt_x(xa0);
+        }
         mcs_wait<D - 1>();
         __syncthreads();
     }
