@@ -19,7 +19,7 @@
 // m-th vertex of that colour in each of the two rows (7 columns apart), so
 // every lane has two independent vertex updates per superstep.
 //
-// Shared memory (one CTA per SM, 8 warps, 211 KB):
+// Shared memory (one CTA per SM, 8 compute warps + 6 duty warps, 211 KB):
 //  * the r ring: 34 rows of (state, adjoint) pairs over the tile plus halo;
 //    a neighbour is one 16-byte access and a vertex's two unknown updates
 //    share one load and one store of its neighbourhood;
@@ -84,7 +84,7 @@ constexpr int WPC = MCS_WPC;
 constexpr int KW = K / WPC;          // rows per colour warp and superstep
 static_assert(K % WPC == 0, "rows per superstep split evenly over a colour's warps");
 #ifndef MCS_ND
-#define MCS_ND 4
+#define MCS_ND 6
 #endif
 // duty warps: they load the rows (cp.async) and write the final ones back
 // while the colour warps compute.  With MCS_ND = 0 every thread shares the
