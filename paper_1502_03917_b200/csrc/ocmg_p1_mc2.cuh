@@ -40,7 +40,8 @@
 //
 // Measured (B200, L12, scripts/kbench.py in-place sweep; scripts/mc2_prof.py
 // per-warp cycle counters with -DMC2_PROF; scripts/micro_node.cu,
-// micro_dfma_lat.cu): 0.67 ms against k_p1_mc_sweep's 0.52 ms.  A vertex
+// micro_dfma_lat.cu): 0.67 ms against k_p1_mc_sweep's 0.44 ms (0.52 before
+// its duty warps).  A vertex
 // update is a 20-deep dependent FP64 chain (DFMA 8.3 cycles): 217 cycles on
 // one warp, 250 for 7 warps with the 3 + 3 shared-memory accesses, 400 with a
 // CTA barrier per step -- the kernel's step takes ~1100, its compute phase
@@ -616,7 +617,7 @@ __global__ void __launch_bounds__(mc2::NT, 1) k_p1_mc_roll(const __grid_constant
 // Which one-launch kernel the multicolour sweep uses: k_p1_mc_sweep, unless
 // OCMG_MC_SWEEP=roll asks for the rolling-window kernel of this file (both
 // are bit-identical to the 7-pass form).  Measured at L12 on a B200
-// (scripts/kbench.py, in-place sweep): ring 0.52 ms, roll 0.67 ms -- see the
+// (scripts/kbench.py, in-place sweep): ring 0.44 ms, roll 0.67 ms -- see the
 // notes at the top of this file and DESIGN.md section 3 for why it is not the
 // default.
 inline bool mc_use_roll() {
