@@ -38,27 +38,30 @@
 // this schedule on the CPU (masks, inheritance, slots, duties) against a
 // plain colour-by-colour sweep.
 //
-// Measured (B200, L12, scripts/kbench.py in-place sweep; scripts/mc2_prof.py
-// per-warp cycle counters with -DMC2_PROF; scripts/micro_node.cu,
-// micro_dfma_lat.cu): 0.67 ms against k_p1_mc_sweep's 0.44 ms (0.52 before
-// its duty warps).  A vertex
-// update is a 20-deep dependent FP64 chain (DFMA 8.3 cycles): 217 cycles on
-// one warp, 250 for 7 warps with the 3 + 3 shared-memory accesses, 400 with a
-// CTA barrier per step -- the kernel's step takes ~1100, its compute phase
-// alone ~650.  What was found and fixed on the way: register-staged x
-// spilled and turned the prefetch into a blocking load (x is staged by
-// cp.async now); any spill costs ~300 cycles because L1 is nearly all shared
-// memory (the boundary warp's class-row updates moved out of the row warps);
-// a code copy per position (static window slots, no register moves) ran 7
-// code paths per scheduler and was slower than one copy with 16 moves;
-// one-warp duties (lane = column mod 32) are latency-bound at 2200-4100
-// cycles a row; __threadfence_block before an arrive is a MEMBAR.SC (~300
-// cycles); hardware named barriers and mbarriers cost the same.  What remains
-// unexplained is the compute phase itself (same instruction stream as the
-// micro-benchmark, 2.5x its time; constant-bank loads of the coefficients
-// that do not fit the uniform registers sit inside the chain).  Two rows per
-// warp and step (two independent chains) would need a 46-row ring, more
-// shared memory than an SM has at this tile width.
+// Measured (B200, L12; bench.py --quick under OCMG_MC_SWEEP=roll, scripts/
+// mc2_prof.py per-warp cycle counters with -DMC2_PROF, scripts/micro_node.cu,
+// micro_dfma_lat.cu): 0.411 ms per sweep (40% of HBM) against k_p1_mc_sweep's
+// 0.350 ms.  A vertex update is a 20-deep dependent FP64 chain (DFMA 8.3
+// cycles): 217 cycles on one warp, 250 for 7 warps with the 3 + 3
+// shared-memory accesses, ~400 with a CTA barrier per step.  The kernel's
+// step takes ~1060 cycles: ~600-700 of compute phase and ~300 between one
+// group's last store and the next group's first load (mbarrier, hardware
+// named barriers and a CTA barrier all measure the same).  Found on the way,
+// each worth 10-40%: register-staged x spilled and turned the prefetch into
+// a blocking load (x is staged by cp.async); any value in local memory costs
+// ~300 cycles per reload because L1 is nearly all shared memory (the loop
+// is at the 80-register limit of 22 warps: setup-only state is parked in
+// shared memory, the boundary warp recomputes its lane state each step);
+// divergent regions around one or two lanes' extra loads / stores cost the
+// warp ~50 cycles each (predicated PTX now); a code copy per colour position
+// (static window slots, no register moves) was slower than one copy with 16
+// moves; one-warp duties (lane = column mod 32) are latency-bound at
+// 2200-4100 cycles a row; __threadfence_block before an arrive is a
+// MEMBAR.SC (~300 cycles).  What would be next is a dependency chain per row
+// warp (row y at step S only needs rows y+2, y+1 at S-1, S-2) instead of a
+// barrier per step, which would also let the warps of a group drift apart.
+// Two rows per warp and step (two independent chains) would need a 46-row
+// ring, more shared memory than an SM has at this tile width.
 #pragma once
 
 #include "ocmg_p1_mc.cuh"
@@ -126,6 +129,20 @@ __device__ __forceinline__ double2 lds2(unsigned a) {
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
     return v;
 }
+// predicated forms (no branch: a divergent region around one or two lanes'
+// extra loads or stores cost the whole warp ~50 cycles each, four of them per
+// vertex ~200 of the compute phase's 650)
+__device__ __forceinline__ void lds2_if(double2 &v, unsigned a, bool p) {
+    asm volatile("{\n.reg .pred q;\nsetp.ne.s32 q, %3, 0;\n@q ld.shared.v2.f64 {%0, %1}, [%2];\n}"
+                 : "+d"(v.x), "+d"(v.y)
+                 : "r"(a), "r"((int)p)
+                 : "memory");
+}
+__device__ __forceinline__ void sts2_if(unsigned a, double2 v, bool p) {
+    asm volatile("{\n.reg .pred q;\nsetp.ne.s32 q, %3, 0;\n@q st.shared.v2.f64 [%0], {%1, %2};\n}" ::"r"(a),
+                 "d"(v.x), "d"(v.y), "r"((int)p)
+                 : "memory");
+}
 __device__ __forceinline__ double lds1(unsigned a) {
     double v;
     asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
@@ -187,7 +204,7 @@ __device__ __forceinline__ void mb_wait(unsigned a, unsigned parity) {
 // before it and only LOOK coefficients are held at a time.
 __device__ __forceinline__ void node_update_pair_s(double2 (&v)[7], unsigned ca, unsigned cb,
                                                    double &pa, double &pb) {
-    constexpr int LOOK = 8, N = 58;
+    constexpr int LOOK = 6, N = 58;
     // use i of an unknown (0..28): W_d, W_{7+d} alternating (0..13), 1/n_diag (14), A_d, A_{7+d} (15..28)
     auto slot = [](int i) {
         const int t = i % 29;
@@ -240,109 +257,6 @@ __device__ __forceinline__ void mc2_boundary_row_vertex(const double *Cc, unsign
     sts2(c - 16, v[2]); sts2(c, v[3]); sts2(c + 16, v[4]);
     sts2(u, v[5]); sts2(u + 16, v[6]);
     if (owned) sts2(ad, make_double2(FWD ? pa : pb, FWD ? pb : pa));
-}
-
-// The boundary warp of a CTA: its own function (not inlined), so that its
-// registers are allocated apart from the row warps' (inlined, its class-row
-// updates pushed loop state of both into local memory, ~300 cycles a reload
-// here: L1 is nearly all shared memory).
-struct Mc2Tile {
-    int n1, X0, X1, Y0, Y1, xl, xr, Ylo, Yhi, S_end;
-    unsigned sm, mb;
-};
-template <bool FWD>
-__device__ __noinline__ void mc2_boundary_warp(const McsParams &P, const Mc2Tile T, int lane, int w) {
-    using namespace mc2;
-    const int n1 = T.n1, X0 = T.X0, X1 = T.X1, Y0 = T.Y0, Y1 = T.Y1, xl = T.xl, xr = T.xr;
-    const int Ylo = T.Ylo, Yhi = T.Yhi, S_end = T.S_end;
-    const unsigned sm = T.sm, mb = T.mb;
-    // ---- the boundary-column warp (no window to keep: its own loop, the
-    // same barriers).  Lane (side, q) takes the vertex of colour position
-    // q (row S - 3q) in the three boundary columns at that side of an
-    // interior row, with its class row from shared memory.
-    const int side = lane / NC, q = lane - side * NC;
-    const bool bside = lane < 2 * NC && !(MC2_X & 8) && (side == 0 ? xl == 0 : xr == n1);
-    const int colour = FWD ? q : NC - 1 - q;
-    const int mg = 2 * (NC - 1 - q) + 1;
-    const int c0 = side == 0 ? 0 : n1 - 3;
-    const int ylo_q = max(max(Ylo, Y0 - mg), 3), yhi_q = min(min(Yhi, Y1 + mg), n1 - 3);
-    const int xlo_q = max(xl, X0 - mg), xhi_q = min(xr, X1 + mg);
-    const unsigned cls_s = sm + CLS_OFF;
-    const bool hasbrow = (Ylo < 3 || Yhi > n1 - 3) && !(MC2_X & 16);
-#ifdef MC2_PROF
-    long long pw = 0, pc = 0, pa = 0;
-    const long long pstart = clock64();
-#endif
-    for (int S = 0; S < S_end; ++S) {
-        MC2_T(t0);
-        if (S > 0) mb_wait(mb + 8u * ((S - 1) % 3), (unsigned)(((S - 1) / 3) & 1));
-        MC2_T(t1);
-        const int rq = S - 3 * q, yb = Ylo + rq;
-        if (bside && rq >= 0 && yb >= ylo_q && yb < yhi_q) {
-            const int ob = pmod7(colour - 2 * yb - c0);
-            const int xb = c0 + ob;
-            if (ob < 3 && xb >= xlo_q && xb < xhi_q) {
-                const unsigned cb = (unsigned)(xb - xl + GL) * 16u;
-                const int sl = rq % RING;  // slot of row yb - 1
-                const unsigned bB = sm + (unsigned)sl * RS + cb;
-                const unsigned bC = sm + (unsigned)((sl + 1) % RING) * RS + cb;
-                const unsigned bU = sm + (unsigned)((sl + 2) % RING) * RS + cb;
-                double2 u[7];
-                u[0] = lds2(bB - 16); u[1] = lds2(bB);
-                u[2] = lds2(bC - 16); u[3] = lds2(bC); u[4] = lds2(bC + 16);
-                u[5] = lds2(bU); u[6] = lds2(bU + 16);
-                const unsigned cs = cls_s + (unsigned)(p1_axis_class(xb, n1) * 2) * (CROW * 8);
-                const unsigned ca = cs + (FWD ? 0 : CROW * 8), cb2 = cs + (FWD ? CROW * 8 : 0);
-                double pa, pb;
-                node_update_pair_s(u, ca, cb2, pa, pb);
-                sts2(bB - 16, u[0]); sts2(bB, u[1]);
-                sts2(bC - 16, u[2]); sts2(bC, u[3]); sts2(bC + 16, u[4]);
-                sts2(bU, u[5]); sts2(bU + 16, u[6]);
-                if ((unsigned)(yb - Y0) < (unsigned)(Y1 - Y0) &&
-                    (unsigned)(xb - X0) < (unsigned)(X1 - X0))
-                    sts2(sm + D_OFF + (unsigned)((rq + 1) % DRING) * DS + (unsigned)(xb - X0) * 16u,
-                         make_double2(FWD ? pa : pb, FWD ? pb : pa));
-            }
-        }
-        // a boundary row (y < 3 or y > n1 - 4) among the rows computed
-        // this step: at most one per end of the domain (they are 3
-        // apart).  Lane = segment, every column with its own class row.
-        if (hasbrow) {
-            for (int qq = 0; qq < NC; ++qq) {
-                const int rr = S - 3 * qq, y = Ylo + rr;
-                if (rr < 0 || y >= Yhi || (unsigned)(y - 3) <= (unsigned)(n1 - 7)) continue;
-                const int mgq = 2 * (NC - 1 - qq) + 1;
-                if (y < max(Ylo, Y0 - mgq) || y >= min(Yhi, Y1 + mgq)) continue;
-                const int x = xl - pmod7(xl + 2 * y) + 7 * lane + (FWD ? qq : 6 - qq);
-                if (x >= max(xl, X0 - mgq) && x < min(xr, X1 + mgq)) {
-                    const unsigned cb = (unsigned)(x - xl + GL) * 16u;
-                    const int sl = rr % RING;  // slot of row y - 1
-                    const unsigned s1 = (unsigned)((sl + 1) % RING);
-                    const double *Cc =
-                        P.C + (7 * p1_axis_class(y, n1) + p1_axis_class(x, n1)) * 58;
-                    mc2_boundary_row_vertex<FWD>(
-                        Cc, sm + (unsigned)sl * RS + cb, sm + s1 * RS + cb,
-                        sm + (unsigned)((sl + 2) % RING) * RS + cb,
-                        sm + D_OFF + (unsigned)((rr + 1) % DRING) * DS + (unsigned)(x - X0) * 16u,
-                        (unsigned)(y - Y0) < (unsigned)(Y1 - Y0) &&
-                            (unsigned)(x - X0) < (unsigned)(X1 - X0));
-                }
-            }
-        }
-        MC2_T(t2);
-        mb_arrive_warp(mb + 8u * (S % 3));
-#ifdef MC2_PROF
-        pw += t1 - t0;
-        pc += t2 - t1;
-        pa += clock64() - t2;
-#endif
-    }
-#ifdef MC2_PROF
-    if (lane == 0) {
-        unsigned long long *o = mc2_prof + ((size_t)blockIdx.x * 24 + w) * 4;
-        o[0] = pw; o[1] = pc; o[2] = pa; o[3] = clock64() - pstart;
-    }
-#endif
 }
 
 template <bool FWD>
@@ -399,8 +313,127 @@ __global__ void __launch_bounds__(mc2::NT, 1) k_p1_mc_roll(const __grid_constant
     __syncthreads();
 
     if (w == NWARP) {
-        const Mc2Tile T{n1, X0, X1, Y0, Y1, xl, xr, Ylo, Yhi, S_end, sm, mb};
-        mc2_boundary_warp<FWD>(P, T, lane, w);
+        // ---- the boundary warp (no window to keep: its own loop, the same
+        // step barriers).  Lane (side, q) takes the vertex of colour position
+        // q (row S - 3q) in the three boundary columns at that side of an
+        // interior row, with its class row from shared memory.  The loop
+        // carries only the lane's window of steps; everything else is
+        // recomputed where there is work (state pushed into local memory
+        // costs ~300 cycles a reload here -- L1 is nearly all shared memory
+        // --, which made this the slowest warp of every step).
+        const int side = lane / NC, q = lane - side * NC;
+        int Slo = 0, Sw = 0;  // steps at which position q has an interior row in its valid range
+        if (lane < 2 * NC && !(MC2_X & 8) && (side == 0 ? xl == 0 : xr == n1)) {
+            const int mg = 2 * (NC - 1 - q) + 1;
+            const int ylo_q = max(max(Ylo, Y0 - mg), 3), yhi_q = min(min(Yhi, Y1 + mg), n1 - 3);
+            Slo = ylo_q - Ylo + 3 * q;
+            Sw = max(yhi_q - ylo_q, 0);
+        }
+        const bool brows = (Ylo < 3 || Yhi > n1 - 3) && !(MC2_X & 16);
+        // the loop's per-lane state lives in shared memory, and the step
+        // counter is parked there across the work (the register allocator
+        // otherwise keeps them in local memory for the whole loop)
+        __shared__ int bw_state[3 * 32];
+        bw_state[lane] = Slo;
+        bw_state[32 + lane] = Sw;
+        const unsigned bw_base = (unsigned)__cvta_generic_to_shared(bw_state);  // CTA-uniform
+        auto lds_i = [](unsigned a) {
+            int v;
+            asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+            return v;
+        };
+#ifdef MC2_PROF
+        long long pw = 0, pc = 0, pa = 0;
+        const long long pstart = clock64();
+#endif
+#pragma unroll 1
+        for (int S = 0; S < S_end; ++S) {
+            MC2_T(t0);
+            if (S > 0) mb_wait(mb + 8u * ((S - 1) % 3), (unsigned)(((S - 1) / 3) & 1));
+            MC2_T(t1);
+            // (lane-derived values are recomputed from %laneid each step
+            // rather than carried: carried, they went to local memory)
+            unsigned lid;
+            asm volatile("mov.u32 %0, %%laneid;" : "=r"(lid));
+            const unsigned bws = bw_base + 4u * lid;
+            const int lane = (int)lid, side = lane / NC, q = lane - side * NC;
+            asm volatile("st.shared.s32 [%0], %1;" ::"r"(bws + 256u), "r"(S) : "memory");
+            if ((unsigned)(S - lds_i(bws)) < (unsigned)lds_i(bws + 128u)) {
+                const int colour = FWD ? q : NC - 1 - q;
+                const int mg = 2 * (NC - 1 - q) + 1;
+                const int c0 = side == 0 ? 0 : n1 - 3;
+                const int xlo_q = max(xl, X0 - mg), xhi_q = min(xr, X1 + mg);
+                const unsigned cls_s = sm + CLS_OFF;
+                const int rq = S - 3 * q, yb = Ylo + rq;
+                const int ob = pmod7(colour - 2 * yb - c0);
+                const int xb = c0 + ob;
+                if (ob < 3 && xb >= xlo_q && xb < xhi_q) {
+                    const unsigned cb = (unsigned)(xb - xl + GL) * 16u;
+                    const int sl = rq % RING;  // slot of row yb - 1
+                    const unsigned bB = sm + (unsigned)sl * RS + cb;
+                    const unsigned bC = sm + (unsigned)((sl + 1) % RING) * RS + cb;
+                    const unsigned bU = sm + (unsigned)((sl + 2) % RING) * RS + cb;
+                    double2 u[7];
+                    u[0] = lds2(bB - 16); u[1] = lds2(bB);
+                    u[2] = lds2(bC - 16); u[3] = lds2(bC); u[4] = lds2(bC + 16);
+                    u[5] = lds2(bU); u[6] = lds2(bU + 16);
+                    const unsigned cs = cls_s + (unsigned)(p1_axis_class(xb, n1) * 2) * (CROW * 8);
+                    const unsigned ca = cs + (FWD ? 0 : CROW * 8), cb2 = cs + (FWD ? CROW * 8 : 0);
+                    double pa, pb;
+                    node_update_pair_s(u, ca, cb2, pa, pb);
+                    sts2(bB - 16, u[0]); sts2(bB, u[1]);
+                    sts2(bC - 16, u[2]); sts2(bC, u[3]); sts2(bC + 16, u[4]);
+                    sts2(bU, u[5]); sts2(bU + 16, u[6]);
+                    if ((unsigned)(yb - Y0) < (unsigned)(Y1 - Y0) &&
+                        (unsigned)(xb - X0) < (unsigned)(X1 - X0))
+                        sts2(sm + D_OFF + (unsigned)((rq + 1) % DRING) * DS + (unsigned)(xb - X0) * 16u,
+                             make_double2(FWD ? pa : pb, FWD ? pb : pa));
+                }
+            }
+            // a boundary row (y < 3 or y > n1 - 4) among the rows computed
+            // this step: at most one per end of the domain (they are 3
+            // apart), and only in the first 3 + 3 * 7 steps of a CTA at the
+            // bottom, from row n1 - 3 on at the top.  Lane = segment, every
+            // column with its own class row.
+            if (brows && (Ylo + S < 3 + 3 * NC || Ylo + S >= n1 - 3)) {
+                for (int qq = 0; qq < NC; ++qq) {
+                        const int rr = S - 3 * qq, y = Ylo + rr;
+                        if (rr < 0 || y >= Yhi || (unsigned)(y - 3) <= (unsigned)(n1 - 7)) continue;
+                        const int mgq = 2 * (NC - 1 - qq) + 1;
+                        if (y < max(Ylo, Y0 - mgq) || y >= min(Yhi, Y1 + mgq)) continue;
+                        const int x = xl - pmod7(xl + 2 * y) + 7 * lane + (FWD ? qq : 6 - qq);
+                        if (x >= max(xl, X0 - mgq) && x < min(xr, X1 + mgq)) {
+                            const unsigned cb = (unsigned)(x - xl + GL) * 16u;
+                            const int sl = rr % RING;  // slot of row y - 1
+                            const unsigned s1 = (unsigned)((sl + 1) % RING);
+                            const double *Cc =
+                                P.C + (7 * p1_axis_class(y, n1) + p1_axis_class(x, n1)) * 58;
+                            mc2_boundary_row_vertex<FWD>(
+                                Cc, sm + (unsigned)sl * RS + cb, sm + s1 * RS + cb,
+                                sm + (unsigned)((sl + 2) % RING) * RS + cb,
+                                sm + D_OFF + (unsigned)((rr + 1) % DRING) * DS + (unsigned)(x - X0) * 16u,
+                                (unsigned)(y - Y0) < (unsigned)(Y1 - Y0) &&
+                                    (unsigned)(x - X0) < (unsigned)(X1 - X0));
+                        }
+                    }
+            }
+            unsigned lid2;  // (again: not carried across the work)
+            asm volatile("mov.u32 %0, %%laneid;" : "=r"(lid2));
+            S = lds_i(bw_base + 256u + 4u * lid2);
+            MC2_T(t2);
+            mb_arrive_warp(mb + 8u * (S % 3));
+#ifdef MC2_PROF
+            pw += t1 - t0;
+            pc += t2 - t1;
+            pa += clock64() - t2;
+#endif
+        }
+#ifdef MC2_PROF
+        if (lane == 0) {
+            unsigned long long *o = mc2_prof + ((size_t)blockIdx.x * 24 + w) * 4;
+            o[0] = pw; o[1] = pc; o[2] = pa; o[3] = clock64() - pstart;
+        }
+#endif
         return;
     }
 
@@ -413,7 +446,7 @@ __global__ void __launch_bounds__(mc2::NT, 1) k_p1_mc_roll(const __grid_constant
     // columns: positions of the segment that are the lane's (in a colour's
     // valid region, not a boundary column) and that the tile owns
     // (packed: bits 0-6 the lane's, 8-14 owned)
-    unsigned cm = 0;
+    unsigned cm = 0;  // (built here, parked in shared memory below)
     {
         const int xs0 = xl - pmod7(xl + 2 * (Ylo + w)) + 7 * lane;
 #pragma unroll
@@ -425,8 +458,15 @@ __global__ void __launch_bounds__(mc2::NT, 1) k_p1_mc_roll(const __grid_constant
         }
     }
     // ring column (bytes) of position 0; the delta column is db_u further
-    const unsigned cb0 =
+    const unsigned cb0_ =
         (unsigned)(xl - pmod7(xl + 2 * (Ylo + w)) + 7 * lane + (FWD ? 0 : 6) - xl + GL) * 16u;
+    // what only the per-row setup needs is parked in shared memory per thread
+    // (2 x 4 bytes): the loop is at the register limit of 22 warps (80), and
+    // a value pushed into local memory costs ~300 cycles per reload
+    __shared__ unsigned park[2 * NWARP * 32];
+    park[tid] = cm;
+    park[NWARP * 32 + tid] = cb0_;
+    const unsigned park_a = (unsigned)__cvta_generic_to_shared(park) + 4u * tid;
     const unsigned db_u = (unsigned)(xl - GL - X0) * 16u;
 
     // compute state
@@ -446,6 +486,9 @@ __global__ void __launch_bounds__(mc2::NT, 1) k_p1_mc_roll(const __grid_constant
     for (int d = 0; d < 7; ++d) v[d] = make_double2(0.0, 0.0);
 
     auto setup = [&]() {  // masks and addresses of row ry
+        unsigned cm, cb0;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cm) : "r"(park_a) : "memory");
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cb0) : "r"(park_a + 4u * NWARP * 32) : "memory");
         const int y = Ylo + ry;
         // (the boundary rows y < 3, y > n1 - 4 are the boundary warp's)
         rowact = ry >= 0 && y < Yhi && (unsigned)(y - 3) <= (unsigned)(n1 - 7);
@@ -467,54 +510,51 @@ __global__ void __launch_bounds__(mc2::NT, 1) k_p1_mc_roll(const __grid_constant
     auto compute = [&](int k) {
         if (!rowact || (MC2_X & 1)) return;  // warp-uniform
         const unsigned dk = (unsigned)((FWD ? k : -k) * 16);
-        const bool own = (mask2 >> (k + 1)) & 1u;
-        const bool prev = (mask2 >> k) & 1u, next = (mask2 >> (k + 2)) & 1u;
+        // (MC2_X timing experiments: 64 every lane owns and inherits, 32 no
+        // window moves, 256 no vertex updates)
+        const bool own = (MC2_X & 64) ? true : (bool)((mask2 >> (k + 1)) & 1u);
+        const bool prev = (MC2_X & 64) ? true : (bool)((mask2 >> k) & 1u);
+        const bool next = (MC2_X & 64) ? true : (bool)((mask2 >> (k + 2)) & 1u);
         const unsigned b = aB + dk, c = aC + dk, u = aU + dk;
         // the three entries that enter the window are loaded by every lane
         // (always inside the ring), so that only the four inherited ones are
         // live from one position to the next
+        const bool full = own && !prev;  // the window is not inherited: load all of it
         if (FWD) {
-            v[0] = v[1]; v[2] = v[3]; v[3] = v[4]; v[5] = v[6];
+            if (!(MC2_X & 32)) { v[0] = v[1]; v[2] = v[3]; v[3] = v[4]; v[5] = v[6]; }
             v[1] = lds2(b); v[4] = lds2(c + 16); v[6] = lds2(u + 16);
-            if (own && !prev) {
-                v[0] = lds2(b - 16); v[2] = lds2(c - 16);
-                v[3] = lds2(c); v[5] = lds2(u);
-            }
+            lds2_if(v[0], b - 16, full); lds2_if(v[2], c - 16, full);
+            lds2_if(v[3], c, full); lds2_if(v[5], u, full);
         } else {
-            v[6] = v[5]; v[4] = v[3]; v[3] = v[2]; v[1] = v[0];
+            if (!(MC2_X & 32)) { v[6] = v[5]; v[4] = v[3]; v[3] = v[2]; v[1] = v[0]; }
             v[0] = lds2(b - 16); v[2] = lds2(c - 16); v[5] = lds2(u);
-            if (own && !prev) {
-                v[1] = lds2(b); v[3] = lds2(c);
-                v[4] = lds2(c + 16); v[6] = lds2(u + 16);
-            }
+            lds2_if(v[1], b, full); lds2_if(v[3], c, full);
+            lds2_if(v[4], c + 16, full); lds2_if(v[6], u + 16, full);
         }
-        const double pa = mcs::node_update_u<FWD ? 0 : 1>(v, P.cu);
-        const double pb = mcs::node_update_u<FWD ? 1 : 0>(v, P.cu);
-        if (own) {
-            if (FWD) {
-                sts2(b - 16, v[0]); sts2(c - 16, v[2]); sts2(u, v[5]);
-                if (!next) {
-                    sts2(b, v[1]); sts2(c, v[3]);
-                    sts2(c + 16, v[4]); sts2(u + 16, v[6]);
-                }
-            } else {
-                sts2(b, v[1]); sts2(c + 16, v[4]); sts2(u + 16, v[6]);
-                if (!next) {
-                    sts2(b - 16, v[0]); sts2(c - 16, v[2]);
-                    sts2(c, v[3]); sts2(u, v[5]);
-                }
-            }
+        double pa = v[3].x, pb = v[3].y;
+        if (!(MC2_X & 256)) {
+            pa = mcs::node_update_u<FWD ? 0 : 1>(v, P.cu);
+            pb = mcs::node_update_u<FWD ? 1 : 0>(v, P.cu);
         }
-        if ((omask >> k) & 1u) sts2(aD + dk, make_double2(FWD ? pa : pb, FWD ? pb : pa));
+        const bool rest = own && !next;  // the next vertex does not inherit: store all of it
+        if (FWD) {
+            sts2_if(b - 16, v[0], own); sts2_if(c - 16, v[2], own); sts2_if(u, v[5], own);
+            sts2_if(b, v[1], rest); sts2_if(c, v[3], rest);
+            sts2_if(c + 16, v[4], rest); sts2_if(u + 16, v[6], rest);
+        } else {
+            sts2_if(b, v[1], own); sts2_if(c + 16, v[4], own); sts2_if(u + 16, v[6], own);
+            sts2_if(b - 16, v[0], rest); sts2_if(c - 16, v[2], rest);
+            sts2_if(c, v[3], rest); sts2_if(u, v[5], rest);
+        }
+        sts2_if(aD + dk, make_double2(FWD ? pa : pb, FWD ? pb : pa),
+                ((omask >> k) & 1u) && !(MC2_X & 128));
     };
 
-    unsigned smod = 0;  // S % RING
     // A thread per column: gt = the thread's index in its group.
     const int gt = m * 32 + lane;
     auto retire = [&](int S) {
         const int R = Ylo + S - RETIRE;
-        const unsigned rslot = smod + (RING - RETIRE + 1) >= RING ? smod + 1 - RETIRE
-                                                                   : smod + (RING - RETIRE + 1);
+        const unsigned rslot = (unsigned)(S + RING - RETIRE + 1) % RING;
         mcs_wait<1>();
         if (gt < X1 - X0 && !(MC2_X & 2)) {
             if (R >= Y0 && R < Y1) {
@@ -544,7 +584,7 @@ __global__ void __launch_bounds__(mc2::NT, 1) k_p1_mc_roll(const __grid_constant
     // arrival at a step barrier publishes it; the x staged just before may
     // still be in flight)
     auto load = [&](int S) {
-        const unsigned lslot = smod + AHEAD + 1 >= RING ? smod + AHEAD + 1 - RING : smod + AHEAD + 1;
+        const unsigned lslot = (unsigned)(S + AHEAD + 1) % RING;
         mcs_wait<1>();
         if (Ylo + S + AHEAD <= Yhi && !(MC2_X & 4)) load_col(gt, S + AHEAD, lslot);
         mcs_commit();
@@ -553,7 +593,6 @@ __global__ void __launch_bounds__(mc2::NT, 1) k_p1_mc_roll(const __grid_constant
     int S = 0;
     auto step = [&]() {
         ++S;
-        smod = smod + 1 == RING ? 0 : smod + 1;
     };
     // the duties of a group run between its compute steps, off the chain of
     // step barriers; they are written for "step S" = the step they would
@@ -572,7 +611,6 @@ __global__ void __launch_bounds__(mc2::NT, 1) k_p1_mc_roll(const __grid_constant
     // virtual row w - 21 (m > 0).
     setup();
     int k = (NC - m) % NC;
-    const unsigned mb_wait_a = mb + 8u * ((grp + 2) % 3), mb_done_a = mb + 8u * grp;
 #ifdef MC2_PROF
     long long pw = 0, pc = 0, pd = 0;
     const long long pstart = clock64();
@@ -580,10 +618,10 @@ __global__ void __launch_bounds__(mc2::NT, 1) k_p1_mc_roll(const __grid_constant
     for (;;) {
         if (S >= S_end) break;
         MC2_T(t0);
-        if (S > 0) mb_wait(mb_wait_a, (unsigned)(((S - 1) / 3) & 1));
+        if (S > 0) mb_wait(mb + 8u * ((unsigned)(S + 2) % 3), (unsigned)(((S - 1) / 3) & 1));
         MC2_T(t1);
         compute(k);
-        mb_arrive_warp(mb_done_a);
+        mb_arrive_warp(mb + 8u * ((unsigned)S % 3));
         MC2_T(t2);
 #ifdef MC2_PROF
         pw += t1 - t0;
@@ -617,7 +655,7 @@ __global__ void __launch_bounds__(mc2::NT, 1) k_p1_mc_roll(const __grid_constant
 // Which one-launch kernel the multicolour sweep uses: k_p1_mc_sweep, unless
 // OCMG_MC_SWEEP=roll asks for the rolling-window kernel of this file (both
 // are bit-identical to the 7-pass form).  Measured at L12 on a B200
-// (scripts/kbench.py, in-place sweep): ring 0.44 ms, roll 0.67 ms -- see the
+// (bench.py --quick): ring 0.350 ms, roll 0.411 ms per sweep -- see the
 // notes at the top of this file and DESIGN.md section 3 for why it is not the
 // default.
 inline bool mc_use_roll() {

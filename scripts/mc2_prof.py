@@ -22,6 +22,15 @@ a = a[live]
 nst = 24
 strip = np.arange(256)[live] % nst
 print("CTAs", a.shape[0])
+tot = a[:, 0, 3]
+segs = np.arange(256)[live] // nst
+print("total cycles by row segment (mean over strips):", [int(tot[segs == s].mean()) for s in range(segs.max() + 1)])
+for s in range(segs.max() + 1):
+    b = a[segs == s]
+    print("  seg", s, "row warps wait %.0f compute %.0f duty %.0f | bw wait %.0f work %.0f arrive %.0f (totals / 1000)" % (
+        b[:, :21, 0].mean() / 1e3, b[:, :21, 1].mean() / 1e3, b[:, :21, 2].mean() / 1e3,
+        b[:, 21, 0].mean() / 1e3, b[:, 21, 1].mean() / 1e3, b[:, 21, 2].mean() / 1e3))
+print("total cycles by strip (mean over segments):", [int(tot[strip == s].mean()) for s in range(nst)])
 for name, sel in (("interior", (strip > 0) & (strip < nst - 1)), ("edge", (strip == 0) | (strip == nst - 1))):
     b = a[sel]
     if not len(b): continue
