@@ -204,6 +204,13 @@ __device__ __forceinline__ double2 mcs_lds2(unsigned a) {
 __device__ __forceinline__ void mcs_sts2(unsigned a, double2 v) {
     asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
 }
+// predicated store (no branch: a divergent region around the stores of the
+// lanes at a tile's edge costs the whole warp ~50 cycles)
+__device__ __forceinline__ void mcs_sts2_if(unsigned a, double2 v, bool p) {
+    asm volatile("{\n.reg .pred q;\nsetp.ne.s32 q, %3, 0;\n@q st.shared.v2.f64 [%0], {%1, %2};\n}" ::"r"(a),
+                 "d"(v.x), "d"(v.y), "r"((int)p)
+                 : "memory");
+}
 // node_update with the coefficient row in shared memory (cs: its address,
 // 16-byte aligned; asm volatile keeps the 15 loads next to their use)
 __device__ __forceinline__ double node_update_s(double2 (&v)[7], unsigned cs) {
@@ -419,22 +426,23 @@ __global__ void __launch_bounds__(mcs::NT, 1) k_p1_mc_sweep(const __grid_constan
             const double pa1 = node_update_u<FWD ? 0 : 1>(v1, cu);
             const double pb0 = node_update_u<FWD ? 1 : 0>(v0, cu);
             const double pb1 = node_update_u<FWD ? 1 : 0>(v1, cu);
-            if ((unsigned)(o - fxlo) < (unsigned)fxw) {
-                mcs_sts2(ra0 + c0 - 16, v0[0]); mcs_sts2(ra0 + c0, v0[1]);
-                mcs_sts2(ra1 + c0 - 16, v0[2]); mcs_sts2(ra1 + c0, v0[3]); mcs_sts2(ra1 + c0 + 16, v0[4]);
-                mcs_sts2(ra2 + c0, v0[5]); mcs_sts2(ra2 + c0 + 16, v0[6]);
-                if ((unsigned)(y - Y0) < (unsigned)(Y1 - Y0) && (unsigned)(o - oxlo) < (unsigned)oxw)
-                    mcs_sts2(xe0, make_double2(__dadd_rn(xo0.x, FWD ? pa0 : pb0),
-                                               __dadd_rn(xo0.y, FWD ? pb0 : pa0)));
-            }
-            if ((unsigned)(o1 - fxlo) < (unsigned)fxw) {
-                mcs_sts2(ra1 + c1 - 16, v1[0]); mcs_sts2(ra1 + c1, v1[1]);
-                mcs_sts2(ra2 + c1 - 16, v1[2]); mcs_sts2(ra2 + c1, v1[3]); mcs_sts2(ra2 + c1 + 16, v1[4]);
-                mcs_sts2(ra3 + c1, v1[5]); mcs_sts2(ra3 + c1 + 16, v1[6]);
-                if ((unsigned)(y + 1 - Y0) < (unsigned)(Y1 - Y0) && (unsigned)(o1 - oxlo) < (unsigned)oxw)
-                    mcs_sts2(xe1, make_double2(__dadd_rn(xo1.x, FWD ? pa1 : pb1),
-                                               __dadd_rn(xo1.y, FWD ? pb1 : pa1)));
-            }
+            const bool a0 = (unsigned)(o - fxlo) < (unsigned)fxw, a1 = (unsigned)(o1 - fxlo) < (unsigned)fxw;
+            mcs_sts2_if(ra0 + c0 - 16, v0[0], a0); mcs_sts2_if(ra0 + c0, v0[1], a0);
+            mcs_sts2_if(ra1 + c0 - 16, v0[2], a0); mcs_sts2_if(ra1 + c0, v0[3], a0);
+            mcs_sts2_if(ra1 + c0 + 16, v0[4], a0);
+            mcs_sts2_if(ra2 + c0, v0[5], a0); mcs_sts2_if(ra2 + c0 + 16, v0[6], a0);
+            mcs_sts2_if(ra1 + c1 - 16, v1[0], a1); mcs_sts2_if(ra1 + c1, v1[1], a1);
+            mcs_sts2_if(ra2 + c1 - 16, v1[2], a1); mcs_sts2_if(ra2 + c1, v1[3], a1);
+            mcs_sts2_if(ra2 + c1 + 16, v1[4], a1);
+            mcs_sts2_if(ra3 + c1, v1[5], a1); mcs_sts2_if(ra3 + c1 + 16, v1[6], a1);
+            mcs_sts2_if(xe0,
+                        make_double2(__dadd_rn(xo0.x, FWD ? pa0 : pb0), __dadd_rn(xo0.y, FWD ? pb0 : pa0)),
+                        a0 && (unsigned)(y - Y0) < (unsigned)(Y1 - Y0) &&
+                            (unsigned)(o - oxlo) < (unsigned)oxw);
+            mcs_sts2_if(xe1,
+                        make_double2(__dadd_rn(xo1.x, FWD ? pa1 : pb1), __dadd_rn(xo1.y, FWD ? pb1 : pa1)),
+                        a1 && (unsigned)(y + 1 - Y0) < (unsigned)(Y1 - Y0) &&
+                            (unsigned)(o1 - oxlo) < (unsigned)oxw);
         } else {
         // 3. vertex updates (independent: same colour, distance >= 3)
         auto rrow = [&](int j) {  // r ring row j (slot sl + j) as double2*
