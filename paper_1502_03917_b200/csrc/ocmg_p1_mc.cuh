@@ -105,7 +105,30 @@ constexpr int CROW = 30;           // class row: W (14), A (14), 1/n_diag, pad
 // discard) up to 19 r entries past a row end, inside the x ring at worst.
 constexpr int X_OFF = RING * RS;
 constexpr int CLS_OFF = X_OFF + RING * XS;
-constexpr int SMEM = CLS_OFF + 7 * 2 * CROW * 8;
+constexpr int FLG_OFF = CLS_OFF + 7 * 2 * CROW * 8;  // progress counters (MCS_CHAIN)
+constexpr int SMEM = FLG_OFF + 64;
+#ifndef MCS_CHAIN
+#define MCS_CHAIN 0
+#endif
+// MCS_CHAIN = 1 (measured, not the default): no CTA barrier per superstep.
+// Every warp publishes the number of supersteps it has finished (release
+// store to a shared counter) and polls only what it reads: colour q at
+// superstep S for colour q-1 (and the boundary warp) at S-1, colour 0 for the
+// rows' loads, the write-back of rows for colour 6, the boundary warp for all
+// colours at S-1.  The idea was that the warps drift apart by up to a
+// superstep, so that one warp's shared-memory burst overlaps another's FMA
+// chains (with the CTA barrier all 7 bursts come first, then all chains:
+// 784 + ~480 cycles).  Bit-identical (L7-L12, strips, fused block), and
+// slower: 0.478 ms per L12 sweep against 0.349 ms -- the release store costs
+// a colour warp ~230 cycles per superstep (ncu: long_sb at the store after
+// MEMBAR.ALL.CTA) and the warps still wait ~200 cycles per superstep for
+// their predecessor, as they did at the barrier.  (With one polling lane per
+// warp it was 0.66 ms: the warp stayed split in two after the poll and
+// executed every superstep twice.)
+constexpr bool CHAIN = MCS_CHAIN != 0 && ND != 0;
+// counters (32-bit, shared): done[q] (q < 7), boundary warp (7), loads landed per duty warp (8 ..)
+constexpr int F_BW = 7, F_LD = 8;
+static_assert(F_LD + ND <= 16, "flag words");
 constexpr int NLD = (2 * STRIDE + 2 * W + NDT - 1) / NDT;  // row-load entries per duty thread
 constexpr int NST = (2 * W + NDT - 1) / NDT;               // row-store pairs per duty thread
 static_assert((W + 2 * H + 6) / 7 <= 31, "one warp per colour-row, lane 31 free");
@@ -211,6 +234,35 @@ __device__ __forceinline__ void mcs_sts2_if(unsigned a, double2 v, bool p) {
                  "d"(v.x), "d"(v.y), "r"((int)p)
                  : "memory");
 }
+// progress counters in shared memory: one warp publishes (its lanes' earlier
+// shared-memory accesses ordered before it through __syncwarp + release), any
+// warp polls
+__device__ __forceinline__ void mcs_flag_set(unsigned a, int v) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0)
+        asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+#ifndef MCS_DUTY_RELEASE
+#define MCS_DUTY_RELEASE 0
+#endif
+#ifndef MCS_POLL_NS
+#define MCS_POLL_NS 0
+#endif
+// the same without a fence of the publishing thread: for a warp whose data
+// was made visible by a barrier it has just passed (the duty warps: a
+// release fence there also waits for their global stores, ~1 us a superstep)
+__device__ __forceinline__ void mcs_flag_set_relaxed(unsigned a, int v) {
+    if ((threadIdx.x & 31) == 0)
+        asm volatile("st.relaxed.cta.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void mcs_flag_wait(unsigned a, int need) {
+    int v;
+    asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    while (v < need) {
+        if (MCS_POLL_NS) __nanosleep(MCS_POLL_NS);
+        asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    }
+}
 // node_update with the coefficient row in shared memory (cs: its address,
 // 16-byte aligned; asm volatile keeps the 15 loads next to their use)
 __device__ __forceinline__ double node_update_s(double2 (&v)[7], unsigned cs) {
@@ -244,6 +296,7 @@ __global__ void __launch_bounds__(mcs::NT, 1) k_p1_mc_sweep(const __grid_constan
     const unsigned sm = (unsigned)__cvta_generic_to_shared(ring);
     char *const smc = reinterpret_cast<char *>(ring);
     auto wrap = [](int j) { return j >= RING ? j - RING : j; };
+    if (tid < 16) reinterpret_cast<int *>(smc + FLG_OFF)[tid] = tid >= F_LD ? 1 : 0;  // rows of superstep 0 land before the first barrier
     {   // class rows (3, c), c = 0..6 = global classes 21..27
         double *ct = reinterpret_cast<double *>(smc + CLS_OFF);
         for (int i = tid; i < 7 * 2 * 29; i += NT) ct[(i / 29) * CROW + i % 29] = P.C[21 * 58 + i];
@@ -347,14 +400,54 @@ __global__ void __launch_bounds__(mcs::NT, 1) k_p1_mc_sweep(const __grid_constan
             sslot = wrap(sslot + 1);
         }
     };
+    const unsigned flg = sm + FLG_OFF;
+    // the tile touches a side of the domain: the boundary warp has work
+    const bool hb = xl == 0 || xr == n1;
     if (ND != 0 && q >= NCW) {
-        // ---- the duty warps' loop: the same barriers as the compute warps'
+        // ---- the duty warps' loop
         mcs_wait<D - 1>();
         __syncthreads();
         for (int S = 0; S < S_end; ++S) {
-            duties();
-            mcs_wait<D - 1>();
-            __syncthreads();
+            if (!CHAIN) {
+                duties();
+                mcs_wait<D - 1>();
+                __syncthreads();
+                continue;
+            }
+            // rows for superstep S + D in (their slots were freed by the
+            // write-back of superstep S - 1: the duty warps' barrier below)
+#pragma unroll
+            for (int i = 0; i < K; ++i) load_row();
+            mcs_commit();
+            // final rows out: final once colour 6 (and the boundary warp) has finished S - 1
+            // (every lane polls, the same word: with one polling lane the warp
+            // stayed split in two for the rest of the iteration and executed
+            // everything twice)
+            mcs_flag_wait(flg + 4u * (NC - 1), S);
+            if (hb) mcs_flag_wait(flg + 4u * F_BW, S);
+#pragma unroll
+            for (int i = 0; i < K; ++i) {
+                if (srow >= Y0 && srow < Y1) {  // CTA-uniform
+#pragma unroll
+                    for (int e = 0; e < NST; ++e)
+                        if (sact[e]) {
+                            const double2 v = mcs_lds2(soff[e] + (unsigned)sslot * srs[e]);
+                            sp[e][0] = v.x;
+                            sp[e][sfs[e]] = v.y;
+                        }
+                }
+#pragma unroll
+                for (int e = 0; e < NST; ++e) sp[e] += n1;
+                ++srow;
+                sslot = wrap(sslot + 1);
+            }
+            mcs_wait<D - 1>();  // the rows of superstep S + 1 have landed (this thread's part)
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * (ND ? ND : 1)) : "memory");
+#if MCS_DUTY_RELEASE
+            mcs_flag_set(flg + 4u * (F_LD + (q - NCW)), S + 2);
+#else
+            mcs_flag_set_relaxed(flg + 4u * (F_LD + (q - NCW)), S + 2);
+#endif
         }
         mcs_wait<0>();
         return;
@@ -406,9 +499,25 @@ __global__ void __launch_bounds__(mcs::NT, 1) k_p1_mc_sweep(const __grid_constan
     unsigned xa0 = sm + X_OFF + (unsigned)wrap(sl + 1) * XS, xa1 = nxt_x(xa0);
     mcs_wait<D - 1>();
     __syncthreads();
+    if (CHAIN && bw && !hb) return;  // no boundary columns in this tile
 
     for (int S = 0; S < S_end; ++S) {
         if (ND == 0) duties();  // 1. rows for superstep S + D in, 2. final rows out
+        if (CHAIN) {
+            // (warp-uniform control flow: every lane polls the same words)
+            if (bw) {  // every colour has finished S - 1
+#pragma unroll
+                for (int j = 0; j < NC; ++j) mcs_flag_wait(flg + 4u * j, S);
+            } else {   // the colour before (and the boundary warp) has finished S - 1
+                if (q > 0) mcs_flag_wait(flg + 4u * (q - 1), S);
+                if (hb) mcs_flag_wait(flg + 4u * F_BW, S);
+                // colour 0: the rows of this superstep have landed
+                if (q == 0) {
+#pragma unroll
+                    for (int j = 0; j < ND; ++j) mcs_flag_wait(flg + 4u * (F_LD + j), S + 1);
+                }
+            }
+        }
         if (kFast && !bw && (unsigned)(y - fyA) < (unsigned)fyW) {
             int o1 = o + 5;
             o1 -= o1 >= 7 ? 7 : 0;
@@ -571,8 +680,12 @@ __global__ void __launch_bounds__(mcs::NT, 1) k_p1_mc_sweep(const __grid_constan
             xa0 = nxt_x(xa1);
             xa1 = nxt_x(xa0);
         }
-        mcs_wait<D - 1>();
-        __syncthreads();
+        if (CHAIN) {
+            mcs_flag_set(flg + 4u * (bw ? F_BW : qq), S + 1);
+        } else {
+            mcs_wait<D - 1>();
+            __syncthreads();
+        }
     }
     mcs_wait<0>();
 }
