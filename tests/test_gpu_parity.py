@@ -82,7 +82,9 @@ def test_ne_jacobi_bitwise(prob, k, alpha):
         ost.sweep(xo, ro)
     assert np.array_equal(host(xd), xo)
     assert np.array_equal(host(rd), ro)
-    assert st.op_count == ost.op_count or prob == "stokes"
+    # (both count 2 nnz per sweep of the exactly assembled operator; the
+    # reference's own Stokes matrix also stores the quadrature's ~1e-17 entries)
+    assert st.op_count == ost.op_count
 
 
 @pytest.mark.parametrize("prob,k,alpha", CASES)
