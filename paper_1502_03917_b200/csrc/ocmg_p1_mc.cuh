@@ -728,12 +728,20 @@ struct McsPlan {
     int nstrips = 0, base = 0, rem = 0, grid = 0;
 };
 
+// rows per segment at least: shorter segments only add pipeline fill (55 rows
+// of halo and lag per CTA), but on the small levels of a cycle (L7-L9) more,
+// shorter CTAs still shorten the sweep while SMs are idle (24 -> 8: L7 41 ->
+// 34 us, L8 44 -> 36, L9 46 -> 37 per sweep; config 3 multicolour 0.297 ->
+// 0.264 s)
+#ifndef MCS_MIN_SEG_ROWS
+#define MCS_MIN_SEG_ROWS 8
+#endif
 inline McsPlan mcs_plan(int n1, int sm_count, int rows = -1) {
     McsPlan p;
     if (rows < 0) rows = n1;
     p.nstrips = (n1 + mcs::W - 1) / mcs::W;  // balanced widths <= W (kernel)
     // segments much shorter than the pipeline fill (H + STORE_LAG rows) waste steps
-    const int max_seg = std::max(1, rows / 24);
+    const int max_seg = std::max(1, rows / MCS_MIN_SEG_ROWS);
     const int total = std::max(p.nstrips, std::min(sm_count, p.nstrips * max_seg));
     p.base = total / p.nstrips;
     p.rem = total % p.nstrips;

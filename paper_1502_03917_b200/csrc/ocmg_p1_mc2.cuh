@@ -671,7 +671,7 @@ inline McsPlan mc_plan(int n1, int sm_count, int rows = -1) {
     McsPlan p;
     if (rows < 0) rows = n1;
     p.nstrips = (n1 + mc2::W - 1) / mc2::W;
-    const int max_seg = std::max(1, rows / 24);
+    const int max_seg = std::max(1, rows / MCS_MIN_SEG_ROWS);
     const int total = std::max(p.nstrips, std::min(sm_count, p.nstrips * max_seg));
     p.base = total / p.nstrips;
     p.rem = total % p.nstrips;
