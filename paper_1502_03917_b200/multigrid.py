@@ -217,6 +217,23 @@ class Multigrid:
         return SolveReport(it, history, converged, time.perf_counter() - t0,
                            seed, diverged)
 
+    def run(self, f=None, tol_kind="rel_residual", **kw):
+        """One entry point for the two stopping rules:
+        tol_kind="l_norm_iterate" is the reference's own protocol
+        (``solve``: zero right-hand side, seeded start, L-norm of the iterate
+        against ``config.tolerance``) and returns its SolveReport;
+        "rel_residual" is the BASELINE protocol (``solve_to_tolerance``:
+        ||f - A x|| / ||f|| against ``tol``) and returns (x, history)."""
+        if tol_kind == "l_norm_iterate":
+            if f is not None:
+                raise ValueError("the l_norm_iterate protocol has a zero right-hand side")
+            return self.solve(**kw)
+        if tol_kind == "rel_residual":
+            if f is None:
+                raise ValueError("the rel_residual protocol needs a right-hand side")
+            return self.solve_to_tolerance(f, **kw)
+        raise ValueError("tol_kind must be 'l_norm_iterate' or 'rel_residual'")
+
     def solve_to_tolerance(self, f, tol=1e-8, max_cycles=300, x=None,
                            use_graph=True):
         """BASELINE.json protocol: x0 = 0 (or ``x``), repeat

@@ -317,6 +317,25 @@ class _RankState:
         self.r2 = [vec(i) if i >= first else None for i in range(L)]
 
 
+def partition(mg, n_gpus=None, collapse_threshold=None):
+    """The strip-partitioned cycle of ``mg`` over ``n_gpus`` ranks.  Under
+    torch.distributed (one process per GPU, torchrun) this process drives its
+    own rank and exchanges over the process group (n_gpus, if given, must be
+    the world size); without it one process drives all n_gpus ranks on its
+    GPU with loopback exchanges (bit-identical to the single-GPU cycle)."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        ws = dist.get_world_size()
+        if n_gpus is not None and n_gpus != ws:
+            raise ValueError(f"n_gpus={n_gpus} but the process group has {ws} ranks")
+        return StripMultigrid(mg, ws, [dist.get_rank()], DistComm(),
+                              collapse_threshold=collapse_threshold)
+    if n_gpus is None or n_gpus < 1:
+        raise ValueError("n_gpus is required outside torch.distributed")
+    return StripMultigrid(mg, n_gpus, list(range(n_gpus)), LoopbackComm(),
+                          collapse_threshold=collapse_threshold)
+
+
 class StripMultigrid:
     """The BASELINE V/W cycle with its fine levels split into row strips
     (SURVEY.md §8(e)).  Levels whose strips would be thinner than the 15
@@ -334,7 +353,11 @@ class StripMultigrid:
     this process drives (one with DistComm; all of them with LoopbackComm).
     """
 
-    def __init__(self, mg, world_size, ranks, comm):
+    def __init__(self, mg, world_size, ranks, comm, collapse_threshold=None):
+        """collapse_threshold: levels with fewer unknowns than this stay on
+        every rank whole (the coarse end of the cycle "collapsed onto a
+        single GPU", SURVEY.md §5 / north_star (4)), on top of the levels
+        whose strips would be thinner than a sweep's ghost rows."""
         cfg = mg.config
         self.jacobi = cfg.smoother.name == "normal"
         if not self.jacobi and (cfg.gs_mode != "multicolour" or
@@ -350,6 +373,11 @@ class StripMultigrid:
         col = ctypes.c_int()
         _lib.call("ocmg_hierarchy_collapsed_level", mg.native().handle, ctypes.byref(col))
         first = max(first, col.value + 1)
+        if collapse_threshold is not None:
+            big = [i for i, s in enumerate(mg.systems) if s.n >= collapse_threshold]
+            if not big:
+                raise ValueError("collapse_threshold leaves no level to partition")
+            first = max(first, big[0])
         if first < 2:
             raise ValueError("partitioned levels must leave a gathered "
                              "sub-hierarchy of at least one smoothed level")

@@ -469,6 +469,28 @@ def test_strip_multigrid_matches_single_gpu(k, ws, cycle, smoother, co):
     assert np.allclose(h1, h2, rtol=1e-12, atol=0)
 
 
+def test_strip_partition_knobs():
+    """n_gpus / collapse_threshold: the loopback partition over 3
+    ranks with every level below L9 kept whole is still the single-GPU cycle
+    bit for bit; tol_kind selects the stopping rule."""
+    from paper_1502_03917_b200.strips import partition
+    cfg = P.CycleConfig(smoother=P.SmootherKind("lsgs"), cycle="v", coarsest_level=3,
+                        gs_mode="multicolour")
+    mg = P.build_solver("poisson", 9, 1e-6, cfg)
+    f = P.baseline_rhs(mg.finest, 0, add_sine=True)
+    x1, h1 = mg.run(f, tol_kind="rel_residual", tol=0.0, max_cycles=2)
+    sm = partition(mg, n_gpus=3, collapse_threshold=mg.finest.n)
+    assert sm.first == len(mg.systems) - 1
+    sm.load(f)
+    sm.solve(tol=0.0, max_cycles=2)
+    torch.cuda.synchronize()
+    assert torch.equal(sm.gather_x(), x1)
+    with pytest.raises(ValueError):
+        mg.run(f, tol_kind="energy")
+    with pytest.raises(ValueError):
+        partition(mg, n_gpus=3, collapse_threshold=10 * mg.finest.n)
+
+
 @pytest.mark.parametrize("prob,kc", [("poisson", 1), ("poisson", 4),
                                      ("stokes", 1), ("stokes", 3)])
 def test_transfers_bitwise(prob, kc):
