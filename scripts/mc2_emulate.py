@@ -10,7 +10,7 @@ import sys
 
 import numpy as np
 
-NC, H, GL, STRIDE, AHEAD, RETIRE, RING, NWARP = 7, 14, 8, 234, 7, 20, 28, 21
+NC, H, GL, STRIDE, AHEAD, RETIRE, RING, NWARP = 7, 14, 8, 234, 7, 21, 33, 21
 OFF = [(-1, -1), (0, -1), (-1, 0), (0, 0), (1, 0), (0, 1), (1, 1)]
 
 

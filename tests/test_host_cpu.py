@@ -197,3 +197,23 @@ def test_table_request_and_renderers():
     import json
     js = json.loads(tab.render("json"))
     assert js["cells"][0]["iterations"] == 11 and js["cells"][1]["converged"] is False
+
+
+def test_rolling_window_schedule_emulation():
+    """The schedule of the experimental rolling-window multicolour kernel
+    (ocmg_p1_mc2.cuh: own masks, window inheritance, ring slots, duties,
+    tile decomposition), emulated on the CPU line by line
+    (scripts/mc2_emulate.py), reproduces a plain colour-by-colour sweep
+    exactly, forward and backward, on tiles with halos on every side."""
+    import os
+    import re
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for args in (("47", "27", "5", "1"), ("47", "27", "5", "0"), ("40", "171", "3", "1")):
+        out = subprocess.run([sys.executable, os.path.join(root, "scripts", "mc2_emulate.py"), *args],
+                             capture_output=True, text=True, timeout=300)
+        assert out.returncode == 0, out.stderr[-2000:]
+        m = re.search(r"max\|dr\| (\S+) nan (\d+) max\|dx\| (\S+)", out.stdout)
+        assert m, out.stdout
+        assert float(m.group(1)) == 0.0 and int(m.group(2)) == 0 and float(m.group(3)) == 0.0, out.stdout
